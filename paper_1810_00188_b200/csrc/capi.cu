@@ -1,0 +1,941 @@
+// capi.cu — implementation of the C-ABI boundary (include/ermc_b200.h).
+//
+// Host orchestration of reference solve() (solver.cpp:82-180) on one B200:
+//   validate (device min/max/positivity pass + host checks, same messages
+//   and order as solver.cpp:39-58) -> T_max -> build_cdfs / planck_mean / QE
+//   on the host (bitwise the reference's) -> multigrid levels (K3) ->
+//   chunked persistent trace (K1) -> per-cell reduce (K2).
+// The only CPU work is O(n_bands * n_quad) table setup; every cell and ray
+// is processed on the GPU. There is no CPU fallback: without a device every
+// solve entry point returns an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ermc_b200.h"
+#include "ermc_b200.hpp"
+#include "host_tables.hpp"
+#include "trace_common.cuh"
+
+namespace ermc_dev {
+int trace_fp64_block();
+int trace_fp64_blocks_per_sm(bool multi);
+cudaError_t launch_trace_fp64(const TraceParams& P, int grid, cudaStream_t s);
+int trace_fp32_block();
+int trace_fp32_blocks_per_sm(bool multi);
+cudaError_t launch_trace_fp32(const TraceParams& P, int grid, cudaStream_t s);
+cudaError_t launch_trace_rays_fp64(const TraceParams& P, int64_t n,
+                                   const int64_t* cells, const uint32_t* rays,
+                                   const double* dirs, RayRecord* out,
+                                   int64_t* level_steps, cudaStream_t s);
+cudaError_t launch_reduce_cells(const double* q_ray, int64_t n_cells, int rays,
+                                double* q_r, double* std_dev, cudaStream_t s);
+cudaError_t launch_restrict(const double* fine, int fnx, int fny, int fnz,
+                            int ratio, double* coarse, int cnx, int cny,
+                            int cnz, cudaStream_t s);
+cudaError_t launch_field_stats(const double* t, int64_t n, double* scratch,
+                               int n_blocks, double* out3, cudaStream_t s);
+cudaError_t launch_uniform(uint64_t h_seed, int64_t n, const uint64_t* cells,
+                           const uint32_t* rays, const uint32_t* draws,
+                           double* out, cudaStream_t s);
+cudaError_t launch_build_iv32(const double* k, const double* ib, int nb,
+                              int nq, int nt, float4* iv, cudaStream_t s);
+cudaError_t launch_to_fp32(const double* src, float* dst, int64_t n,
+                           cudaStream_t s);
+}  // namespace ermc_dev
+
+using ermc::Error;
+
+namespace {
+
+constexpr int kStatsBlocks = 592;  // 4 x 148 SMs
+
+uint64_t mix64_host(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+void put_err(char* buf, size_t len, const std::string& msg) {
+  if (!buf || len == 0) return;
+  std::snprintf(buf, len, "%s", msg.c_str());
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(std::string("CUDA error in ") + what + ": " +
+                cudaGetErrorString(e));
+}
+
+// RAII device-current switch.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    reset();
+    cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)),
+               "cudaMalloc");
+    n = count;
+  }
+  void upload(const T* src, size_t count, cudaStream_t s) {
+    ensure(count);
+    if (count)
+      cuda_check(cudaMemcpyAsync(p, src, count * sizeof(T),
+                                 cudaMemcpyHostToDevice, s),
+                 "cudaMemcpyAsync H2D");
+  }
+};
+
+void validate_config(const ermc_config_t& c) {
+  // SolveConfig::validate (solver.cpp:14-23)
+  if (c.rays_per_cell < 1) throw Error("SolveConfig: rays_per_cell must be >= 1");
+  if (!(c.tolerance > 0.0 && c.tolerance < 1.0))
+    throw Error("SolveConfig: tolerance must be in (0,1)");
+  if (c.n_levels < 1) throw Error("SolveConfig: n_levels must be >= 1");
+  if (c.steps_per_level < 1)
+    throw Error("SolveConfig: steps_per_level must be >= 1");
+  if (c.max_steps < 1) throw Error("SolveConfig: max_steps must be >= 1");
+  if (c.workers < 0) throw Error("SolveConfig: workers must be >= 0");
+  if (c.precision != ERMC_PRECISION_FP64 && c.precision != ERMC_PRECISION_FP32)
+    throw Error("SolveConfig: precision must be fp64 (0) or fp32 (1)");
+  if (c.n_levels > ermc_dev::kMaxLevels)
+    throw Error("SolveConfig: n_levels above the GPU limit of " +
+                std::to_string(ermc_dev::kMaxLevels));
+}
+
+void validate_grid(const ermc_grid_t& g) {
+  // CartesianGrid::validate (geometry.cpp:15-20)
+  if (g.nx < 1 || g.ny < 1 || g.nz < 1)
+    throw Error("CartesianGrid: cell counts must be >= 1");
+  if (g.dx <= 0.0 || g.dy <= 0.0 || g.dz <= 0.0)
+    throw Error("CartesianGrid: spacings must be positive");
+}
+
+void validate_boundary(const ermc_boundary_t& b) {
+  // BoundarySpec::validate (geometry.cpp:22-32)
+  for (int a = 0; a < 3; ++a) {
+    if (b.kind[a] == ERMC_AXIS_PERIODIC) continue;
+    const double t[2] = {b.lo_temperature[a], b.hi_temperature[a]};
+    const double e[2] = {b.lo_emissivity[a], b.hi_emissivity[a]};
+    for (int s = 0; s < 2; ++s) {
+      if (e[s] < 0.0 || e[s] > 1.0)
+        throw Error("BoundarySpec: wall emissivity must be in [0,1]");
+      if (t[s] < 0.0) throw Error("BoundarySpec: wall temperature must be >= 0");
+    }
+  }
+}
+
+double spacing(const ermc_grid_t& g, int a) {
+  return a == 0 ? g.dx : a == 1 ? g.dy : g.dz;
+}
+int count(const ermc_grid_t& g, int a) { return a == 0 ? g.nx : a == 1 ? g.ny : g.nz; }
+int64_t cells_of(const ermc_grid_t& g) {
+  return static_cast<int64_t>(g.nx) * g.ny * g.nz;
+}
+
+struct Timing {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace
+
+struct ermc_session {
+  int device = 0;
+  int n_sm = 148;
+  ermc_grid_t grid{};
+  ermc_boundary_t boundary{};
+  ermc_config_t config{};
+  // owning host copies of the model tables
+  std::vector<double> nu_lo, nu_hi, nu_c, gp, gw, temps, k, ib;
+  ermc_model_t model{};
+  ermc_host::TableView view;
+  int64_t n_cells = 0;
+
+  DevBuf<double> d_temps, d_k, d_ib, d_wall_ib, d_band_cdf, d_quad_cdf, d_kmax,
+      d_ibmax;
+  DevBuf<float> d_wall_ibn32;
+  DevBuf<double> d_field;
+  std::vector<std::unique_ptr<DevBuf<double>>> d_levels;  // levels >= 1
+  std::vector<ermc_grid_t> level_grids;
+  DevBuf<float> d_field32;
+  std::vector<std::unique_ptr<DevBuf<float>>> d_levels32;
+  DevBuf<float4> d_iv32;
+  bool iv32_ready = false;
+  DevBuf<double> d_qray;
+  DevBuf<unsigned long long> d_counters;  // per chunk: work, err key
+  DevBuf<int32_t> d_errcode;
+  DevBuf<unsigned long long> d_steps;
+  DevBuf<double> d_stats_scratch, d_stats;
+  bool field_set = false;
+  bool levels_valid = false;  // coarse levels match the current field
+
+  double ms[4] = {0, 0, 0, 0};
+  int32_t launches = 0;
+  std::mutex mu;
+  size_t qray_budget_bytes = 0;
+};
+
+namespace {
+
+void copy_model(ermc_session* s, const ermc_model_t& m) {
+  s->nu_lo.assign(m.band_nu_lo, m.band_nu_lo + m.n_bands);
+  s->nu_hi.assign(m.band_nu_hi, m.band_nu_hi + m.n_bands);
+  s->nu_c.assign(m.band_nu_center, m.band_nu_center + m.n_bands);
+  s->gp.assign(m.g_points, m.g_points + m.n_quad);
+  s->gw.assign(m.g_weights, m.g_weights + m.n_quad);
+  s->temps.assign(m.temp_grid, m.temp_grid + m.n_temps);
+  const size_t nk = static_cast<size_t>(m.n_bands) * m.n_quad * m.n_temps;
+  s->k.assign(m.k_table, m.k_table + nk);
+  s->ib.assign(m.ib_table, m.ib_table + static_cast<size_t>(m.n_bands) * m.n_temps);
+  s->model = m;
+  s->model.band_nu_lo = s->nu_lo.data();
+  s->model.band_nu_hi = s->nu_hi.data();
+  s->model.band_nu_center = s->nu_c.data();
+  s->model.g_points = s->gp.data();
+  s->model.g_weights = s->gw.data();
+  s->model.temp_grid = s->temps.data();
+  s->model.k_table = s->k.data();
+  s->model.ib_table = s->ib.data();
+  s->view = ermc_host::make_view_unchecked(s->model);
+}
+
+ermc_session* create_session(const ermc_grid_t* grid,
+                             const ermc_boundary_t* boundary,
+                             const ermc_model_t* model,
+                             const ermc_config_t* config) {
+  if (!grid || !boundary || !model || !config)
+    throw Error("ermc_b200: null descriptor");
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+    cudaGetLastError();
+    throw Error("ermc_b200: no CUDA device available (the solver has no CPU path)");
+  }
+  ermc_host::make_view(*model);  // SpectralModel constructor checks
+  validate_config(*config);
+  validate_grid(*grid);
+  auto s = std::make_unique<ermc_session>();
+  int dev = config->device;
+  if (dev < 0) cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev >= n_dev) throw Error("ermc_b200: device ordinal out of range");
+  s->device = dev;
+  DeviceGuard guard(dev);
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+  s->n_sm = prop.multiProcessorCount;
+  s->grid = *grid;
+  s->boundary = *boundary;
+  s->config = *config;
+  copy_model(s.get(), *model);
+  s->n_cells = cells_of(*grid);
+  size_t free_b = 0, total_b = 0;
+  cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  s->qray_budget_bytes = std::min<size_t>(free_b / 4, size_t(16) << 30);
+
+  cudaStream_t st = nullptr;
+  s->d_temps.upload(s->temps.data(), s->temps.size(), st);
+  s->d_k.upload(s->k.data(), s->k.size(), st);
+  s->d_ib.upload(s->ib.data(), s->ib.size(), st);
+  s->d_field.ensure(static_cast<size_t>(s->n_cells));
+  s->d_stats_scratch.ensure(3 * kStatsBlocks);
+  s->d_stats.ensure(3);
+  s->d_steps.ensure(ermc_dev::kMaxLevels);
+  cuda_check(cudaStreamSynchronize(st), "upload tables");
+  return s.release();
+}
+
+// Per-level grids of build_hierarchy (geometry.cpp:84-110), host side.
+std::vector<ermc_grid_t> level_grids(const ermc_grid_t& g0, int n_levels,
+                                     int ratio) {
+  std::vector<ermc_grid_t> out{g0};
+  if (n_levels > 1 && ratio < 2)
+    throw Error("build_hierarchy: ratio must be >= 2");
+  for (int l = 1; l < n_levels; ++l) {
+    const ermc_grid_t& f = out.back();
+    if (f.nx == 1 && f.ny == 1 && f.nz == 1)
+      throw Error("build_hierarchy: cannot coarsen below one cell; achievable "
+                  "depth is " + std::to_string(l));
+    ermc_grid_t c = f;
+    c.nx = (f.nx + ratio - 1) / ratio;
+    c.ny = (f.ny + ratio - 1) / ratio;
+    c.nz = (f.nz + ratio - 1) / ratio;
+    c.dx = (f.nx * f.dx) / c.nx;  // fg.extent(0) / cg.nx
+    c.dy = (f.ny * f.dy) / c.ny;
+    c.dz = (f.nz * f.dz) / c.nz;
+    out.push_back(c);
+  }
+  return out;
+}
+
+struct Prepared {
+  ermc_dev::TraceParams P{};
+  double t_max = 0.0;
+  double qe = 0.0;
+  std::vector<double> band_cdf, quad_cdf, kmax, ibmax, wall_ib;
+  std::vector<float> wall_ibn32;
+};
+
+// Device stats pass + the reference's validation order (solver.cpp:39-58)
+// for the field-dependent checks; returns T_max (solver.cpp:27-37).
+double validate_field_and_tmax(ermc_session* s, cudaStream_t st) {
+  Timing t;
+  cudaEventCreate(&t.a);
+  cudaEventCreate(&t.b);
+  cudaEventRecord(t.a, st);
+  cuda_check(ermc_dev::launch_field_stats(s->d_field.p, s->n_cells,
+                                          s->d_stats_scratch.p, kStatsBlocks,
+                                          s->d_stats.p, st),
+             "field_stats");
+  s->launches += 2;
+  cudaEventRecord(t.b, st);
+  double h[3];
+  cuda_check(cudaMemcpyAsync(h, s->d_stats.p, sizeof(h), cudaMemcpyDeviceToHost, st),
+             "stats D2H");
+  cuda_check(cudaStreamSynchronize(st), "stats sync");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t.a, t.b);
+  s->ms[0] += ms;
+  cudaEventDestroy(t.a);
+  cudaEventDestroy(t.b);
+  const double fmin_v = h[0], fmax_v = h[1];
+  if (h[2] > 0.0) throw Error("TemperatureField: temperatures must be positive");
+  validate_boundary(s->boundary);
+  const double lo = s->temps.front(), hi = s->temps.back();
+  if (fmin_v < lo || fmax_v > hi)
+    throw Error("solve: field temperatures outside spectral table range");
+  const ermc_boundary_t& b = s->boundary;
+  for (int a = 0; a < 3; ++a) {
+    if (b.kind[a] == ERMC_AXIS_PERIODIC) continue;
+    for (double wt : {b.lo_temperature[a], b.hi_temperature[a]})
+      if (wt != 0.0 && (wt < lo || wt > hi))
+        throw Error("solve: wall temperature outside spectral table range");
+  }
+  double t_max = fmax_v;
+  for (int a = 0; a < 3; ++a) {
+    if (b.kind[a] == ERMC_AXIS_PERIODIC) continue;
+    t_max = std::max({t_max, b.lo_temperature[a], b.hi_temperature[a]});
+  }
+  return t_max;
+}
+
+// Host setup for a given T_max and QE: CDFs, T_max interpolants, wall
+// blackbodies, level descriptors (restricting coarse levels on device).
+void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
+             bool build_levels, cudaStream_t st) {
+  const ermc_host::TableView& v = s->view;
+  const ermc_config_t& c = s->config;
+  pr.t_max = t_max;
+  pr.qe = qe;
+  pr.band_cdf.assign(v.nb, 0.0);
+  pr.quad_cdf.assign(static_cast<size_t>(v.nb) * v.nq, 0.0);
+  ermc_host::build_cdfs(v, t_max, pr.band_cdf.data(), pr.quad_cdf.data());
+  std::vector<ermc_grid_t> grids = level_grids(s->grid, c.n_levels, c.coarsen_ratio);
+
+  pr.kmax.resize(static_cast<size_t>(v.nb) * v.nq);
+  pr.ibmax.resize(v.nb);
+  for (int n = 0; n < v.nb; ++n) {
+    pr.ibmax[n] = ermc_host::interp_ib(v, n, t_max);
+    for (int g = 0; g < v.nq; ++g)
+      pr.kmax[static_cast<size_t>(n) * v.nq + g] = ermc_host::interp_k(v, n, g, t_max);
+  }
+  pr.wall_ib.assign(6 * static_cast<size_t>(v.nb), 0.0);
+  const ermc_boundary_t& b = s->boundary;
+  for (int a = 0; a < 3; ++a) {
+    if (b.kind[a] == ERMC_AXIS_PERIODIC) continue;
+    const double wt[2] = {b.lo_temperature[a], b.hi_temperature[a]};
+    for (int side = 0; side < 2; ++side)
+      if (wt[side] > 0.0)
+        for (int n = 0; n < v.nb; ++n)
+          pr.wall_ib[(2 * a + side) * static_cast<size_t>(v.nb) + n] =
+              ermc_host::interp_ib(v, n, wt[side]);
+  }
+  s->d_band_cdf.upload(pr.band_cdf.data(), pr.band_cdf.size(), st);
+  s->d_quad_cdf.upload(pr.quad_cdf.data(), pr.quad_cdf.size(), st);
+  s->d_kmax.upload(pr.kmax.data(), pr.kmax.size(), st);
+  s->d_ibmax.upload(pr.ibmax.data(), pr.ibmax.size(), st);
+  s->d_wall_ib.upload(pr.wall_ib.data(), pr.wall_ib.size(), st);
+  // fp32 kernel: wall blackbodies normalised like its interval table.
+  pr.wall_ibn32.assign(pr.wall_ib.size(), 0.0f);
+  for (int f = 0; f < 6; ++f)
+    for (int n = 0; n < v.nb; ++n) {
+      const double last = v.ib_node(n, v.nt - 1);
+      const size_t i = static_cast<size_t>(f) * v.nb + n;
+      pr.wall_ibn32[i] = last > 0.0 ? static_cast<float>(pr.wall_ib[i] / last) : 0.0f;
+    }
+  s->d_wall_ibn32.upload(pr.wall_ibn32.data(), pr.wall_ibn32.size(), st);
+
+  // Multigrid levels (K3), restricted level by level like build_hierarchy.
+  if (build_levels && !s->levels_valid) {
+    Timing t;
+    cudaEventCreate(&t.a);
+    cudaEventCreate(&t.b);
+    cudaEventRecord(t.a, st);
+    s->d_levels.resize(grids.size());
+    for (size_t l = 1; l < grids.size(); ++l) {
+      if (!s->d_levels[l]) s->d_levels[l] = std::make_unique<DevBuf<double>>();
+      s->d_levels[l]->ensure(static_cast<size_t>(cells_of(grids[l])));
+      const double* fine = l == 1 ? s->d_field.p : s->d_levels[l - 1]->p;
+      const ermc_grid_t& f = grids[l - 1];
+      const ermc_grid_t& cg = grids[l];
+      cuda_check(ermc_dev::launch_restrict(fine, f.nx, f.ny, f.nz,
+                                           c.coarsen_ratio, s->d_levels[l]->p,
+                                           cg.nx, cg.ny, cg.nz, st),
+                 "restrict");
+      ++s->launches;
+    }
+    cudaEventRecord(t.b, st);
+    cudaEventSynchronize(t.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    s->ms[1] += ms;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+    s->levels_valid = true;
+    s->level_grids = grids;
+  }
+
+  ermc_dev::TraceParams& P = pr.P;
+  std::memset(&P, 0, sizeof(P));
+  P.n_levels = c.n_levels;
+  for (int a = 0; a < 3; ++a) P.periodic[a] = b.kind[a] == ERMC_AXIS_PERIODIC;
+  for (int l = 0; l < c.n_levels; ++l) {
+    const ermc_grid_t& g = grids[l];
+    ermc_dev::LevelDesc& L = P.lv[l];
+    for (int a = 0; a < 3; ++a) {
+      L.n[a] = count(g, a);
+      L.d[a] = spacing(g, a);
+      L.origin[a] = g.origin[a];
+      L.extent[a] = count(g, a) * spacing(g, a);
+    }
+    L.eps = 1e-12 * std::min({g.dx, g.dy, g.dz});
+    L.cap = (l + 1 == c.n_levels) ? -1 : c.steps_per_level;
+    L.field = l == 0 ? s->d_field.p : (s->d_levels.size() > size_t(l) && s->d_levels[l] ? s->d_levels[l]->p : nullptr);
+    L.field32 = nullptr;
+  }
+  for (int a = 0; a < 3; ++a) {
+    P.wall_eps[2 * a] = b.lo_emissivity[a];
+    P.wall_eps[2 * a + 1] = b.hi_emissivity[a];
+  }
+  P.wall_ib = s->d_wall_ib.p;
+  P.wall_ibn32 = s->d_wall_ibn32.p;
+  P.n_bands = v.nb;
+  P.n_quad = v.nq;
+  P.n_temps = v.nt;
+  P.uniform_temps = v.uniform ? 1 : 0;
+  P.t0 = v.t0;
+  P.dt = v.dt;
+  P.temps = s->d_temps.p;
+  P.k = s->d_k.p;
+  P.ib = s->d_ib.p;
+  P.band_cdf = s->d_band_cdf.p;
+  P.quad_cdf = s->d_quad_cdf.p;
+  P.k_max = s->d_kmax.p;
+  P.ib_max = s->d_ibmax.p;
+  P.qe = qe;
+  P.tol = c.tolerance;
+  P.max_steps = c.max_steps;
+  P.specular = c.specular_walls;
+  P.volume_sampling = c.volume_sampling;
+  P.h_seed = mix64_host(c.seed + 0x9e3779b97f4a7c15ULL);
+  P.rays = c.rays_per_cell;
+  P.refill_threshold = 4;
+  P.steps_per_level = s->d_steps.p;
+}
+
+double q_emission(const ermc_session* s, double t_max) {
+  // solver.cpp:90-93
+  const double kp = ermc_host::planck_mean(s->view, t_max);
+  return 4.0 * kp * ermc::kSigma * t_max * t_max * t_max * t_max /
+         s->config.rays_per_cell;
+}
+
+std::string error_message(const ermc_session* s, const ermc_dev::RayRecord& r,
+                          int64_t cell, uint32_t ray) {
+  switch (r.err) {
+    case ermc_dev::kErrNonFinite:
+      return "march: non-finite value at cell " + std::to_string(cell) +
+             " ray " + std::to_string(ray) + " step " + std::to_string(r.steps);
+    case ermc_dev::kErrTableRange:
+      return "temperature " + ermc_host::fmt_double(r.err_value) +
+             " K outside table range [" + ermc_host::fmt_double(s->temps.front()) +
+             ", " + ermc_host::fmt_double(s->temps.back()) + "]";
+    case ermc_dev::kErrTransparent:
+      return "init_ray: sampled a transparent point at T_max; spectral tables "
+             "are inconsistent with the sampling CDFs";
+    case ermc_dev::kErrLocate:
+      return "locate: point outside domain on axis " + std::to_string(r.err_axis);
+    default:
+      return "ermc_b200: device error " + std::to_string(r.err);
+  }
+}
+
+// Re-traces one failing ray with the debug kernel to recover the message.
+std::string describe_failure(ermc_session* s, const ermc_dev::TraceParams& P,
+                             int64_t cell, uint32_t ray, cudaStream_t st) {
+  DevBuf<int64_t> dc;
+  DevBuf<uint32_t> dr;
+  DevBuf<ermc_dev::RayRecord> drec;
+  dc.upload(&cell, 1, st);
+  dr.upload(&ray, 1, st);
+  drec.ensure(1);
+  cuda_check(ermc_dev::launch_trace_rays_fp64(P, 1, dc.p, dr.p, nullptr, drec.p,
+                                              nullptr, st),
+             "trace_rays");
+  ermc_dev::RayRecord rec{};
+  cuda_check(cudaMemcpyAsync(&rec, drec.p, sizeof(rec), cudaMemcpyDeviceToHost, st),
+             "D2H");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  return error_message(s, rec, cell, ray);
+}
+
+void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
+                        cudaStream_t st);
+
+// Core solve of [lo, hi) into device outputs.
+void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
+                        double* d_sd, int64_t* steps_out, cudaStream_t st) {
+  if (!s->field_set) throw Error("ermc_b200: temperature field not set");
+  if (lo < 0 || hi > s->n_cells || lo > hi)
+    throw Error("ermc_b200: cell range outside the grid");
+  for (double& m : s->ms) m = 0.0;
+  s->launches = 0;
+  DeviceGuard guard(s->device);
+  const double t_max = validate_field_and_tmax(s, st);
+  Prepared pr;
+  // build_cdfs (inside prepare) may throw before the hierarchy checks, as
+  // in solver.cpp:88-96; planck_mean cannot fail for an in-range T_max.
+  const double qe = q_emission(s, t_max);
+  prepare(s, pr, t_max, qe, /*build_levels=*/true, st);
+  ermc_dev::TraceParams& P = pr.P;
+  const bool fp32 = s->config.precision == ERMC_PRECISION_FP32;
+  if (fp32) ensure_fp32_inputs(s, P, st);
+
+  const int R = s->config.rays_per_cell;
+  const int64_t total_cells = hi - lo;
+  // Chunk so the per-ray buffer stays within budget and work ids fit 31 bits.
+  const uint64_t max_items = std::min<uint64_t>(
+      (1ull << 31) - 1, std::max<uint64_t>(s->qray_budget_bytes / sizeof(double), R));
+  int64_t chunk_cells = std::max<int64_t>(1, static_cast<int64_t>(max_items / R));
+  chunk_cells = std::min<int64_t>(chunk_cells, std::max<int64_t>(total_cells, 1));
+  const int64_t n_chunks = total_cells == 0 ? 0 : (total_cells + chunk_cells - 1) / chunk_cells;
+  s->d_qray.ensure(static_cast<size_t>(chunk_cells) * R);
+  s->d_counters.ensure(2 * std::max<int64_t>(n_chunks, 1));
+  s->d_errcode.ensure(std::max<int64_t>(n_chunks, 1));
+  cuda_check(cudaMemsetAsync(s->d_counters.p, 0,
+                             2 * std::max<int64_t>(n_chunks, 1) * sizeof(unsigned long long), st),
+             "memset");
+  cuda_check(cudaMemsetAsync(s->d_errcode.p, 0, std::max<int64_t>(n_chunks, 1) * sizeof(int32_t), st),
+             "memset");
+  cuda_check(cudaMemsetAsync(s->d_steps.p, 0, ermc_dev::kMaxLevels * sizeof(unsigned long long), st),
+             "memset");
+  const bool multi = s->config.n_levels > 1;
+  const int bps = fp32 ? ermc_dev::trace_fp32_blocks_per_sm(multi)
+                       : ermc_dev::trace_fp64_blocks_per_sm(multi);
+  const int grid = std::max(1, bps) * s->n_sm;
+
+  std::vector<Timing> tt(n_chunks), tr(n_chunks);
+  for (int64_t ch = 0; ch < n_chunks; ++ch) {
+    const int64_t c0 = lo + ch * chunk_cells;
+    const int64_t nc = std::min<int64_t>(chunk_cells, hi - c0);
+    P.cell_base = c0;
+    P.n_cells = nc;
+    P.n_work = static_cast<uint64_t>(nc) * R;
+    P.work_counter = s->d_counters.p + 2 * ch;
+    P.err_key = s->d_counters.p + 2 * ch + 1;
+    P.err_code = s->d_errcode.p + ch;
+    P.q_ray = s->d_qray.p;
+    cudaEventCreate(&tt[ch].a);
+    cudaEventCreate(&tt[ch].b);
+    cudaEventCreate(&tr[ch].a);
+    cudaEventCreate(&tr[ch].b);
+    cudaEventRecord(tt[ch].a, st);
+    cuda_check(fp32 ? ermc_dev::launch_trace_fp32(P, grid, st)
+                    : ermc_dev::launch_trace_fp64(P, grid, st),
+               "trace");
+    cudaEventRecord(tt[ch].b, st);
+    cudaEventRecord(tr[ch].a, st);
+    cuda_check(ermc_dev::launch_reduce_cells(s->d_qray.p, nc, R, d_q + (c0 - lo),
+                                             d_sd + (c0 - lo), st),
+               "reduce");
+    cudaEventRecord(tr[ch].b, st);
+    s->launches += 2;
+  }
+  std::vector<unsigned long long> counters(2 * std::max<int64_t>(n_chunks, 1));
+  std::vector<int32_t> codes(std::max<int64_t>(n_chunks, 1));
+  unsigned long long steps[ermc_dev::kMaxLevels];
+  cuda_check(cudaMemcpyAsync(counters.data(), s->d_counters.p,
+                             counters.size() * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st),
+             "D2H");
+  cuda_check(cudaMemcpyAsync(codes.data(), s->d_errcode.p, codes.size() * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, st),
+             "D2H");
+  cuda_check(cudaMemcpyAsync(steps, s->d_steps.p, sizeof(steps), cudaMemcpyDeviceToHost, st),
+             "D2H");
+  cuda_check(cudaStreamSynchronize(st), "trace sync");
+  for (int64_t ch = 0; ch < n_chunks; ++ch) {
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, tt[ch].a, tt[ch].b);
+    cudaEventElapsedTime(&b, tr[ch].a, tr[ch].b);
+    s->ms[2] += a;
+    s->ms[3] += b;
+    cudaEventDestroy(tt[ch].a);
+    cudaEventDestroy(tt[ch].b);
+    cudaEventDestroy(tr[ch].a);
+    cudaEventDestroy(tr[ch].b);
+  }
+  for (int64_t ch = 0; ch < n_chunks; ++ch) {
+    const unsigned long long key = counters[2 * ch + 1];
+    if (key == 0ull) continue;
+    const int64_t c0 = lo + ch * chunk_cells;
+    const uint64_t w = key - 1;
+    const int64_t cell = c0 + static_cast<int64_t>(w / R);
+    const uint32_t ray = static_cast<uint32_t>(w % R);
+    // Describe with the fp64 debug tracer (reference arithmetic).
+    P.lv[0].field = s->d_field.p;
+    throw Error(describe_failure(s, P, cell, ray, st));
+  }
+  for (int l = 0; l < s->config.n_levels; ++l)
+    steps_out[l] = static_cast<int64_t>(steps[l]);
+}
+
+void set_field_impl(ermc_session* s, const double* t, int is_device,
+                    cudaStream_t st) {
+  DeviceGuard guard(s->device);
+  s->d_field.ensure(static_cast<size_t>(s->n_cells));
+  cuda_check(cudaMemcpyAsync(s->d_field.p, t, s->n_cells * sizeof(double),
+                             is_device ? cudaMemcpyDeviceToDevice
+                                       : cudaMemcpyHostToDevice,
+                             st),
+             "set_field copy");
+  s->field_set = true;
+  s->levels_valid = false;
+  s->iv32_ready = s->iv32_ready;  // tables unchanged
+  s->d_levels32.clear();
+  s->d_field32.reset();
+}
+
+void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
+                        cudaStream_t st) {
+  const ermc_host::TableView& v = s->view;
+  if (v.nt < 2 || !v.uniform)
+    throw Error("ermc_b200: the fp32 kernel needs a uniform temperature grid "
+                "with at least 2 nodes; use precision=fp64");
+  for (const ermc_grid_t& g : s->level_grids)
+    if (cells_of(g) >= (int64_t(1) << 31))
+      throw Error("ermc_b200: the fp32 kernel supports grids below 2^31 "
+                  "cells; use precision=fp64");
+  if (!s->iv32_ready) {
+    s->d_iv32.ensure(static_cast<size_t>(v.nb) * v.nq * (v.nt - 1));
+    cuda_check(ermc_dev::launch_build_iv32(s->d_k.p, s->d_ib.p, v.nb, v.nq, v.nt,
+                                           s->d_iv32.p, st),
+               "build_iv32");
+    ++s->launches;
+    s->iv32_ready = true;
+  }
+  if (!s->d_field32.p) {
+    s->d_field32.ensure(static_cast<size_t>(s->n_cells));
+    cuda_check(ermc_dev::launch_to_fp32(s->d_field.p, s->d_field32.p, s->n_cells, st),
+               "to_fp32");
+    ++s->launches;
+  }
+  P.lv[0].field32 = s->d_field32.p;
+  s->d_levels32.resize(s->config.n_levels);
+  for (int l = 1; l < s->config.n_levels; ++l) {
+    const int64_t n = cells_of(s->level_grids[l]);
+    if (!s->d_levels32[l]) {
+      s->d_levels32[l] = std::make_unique<DevBuf<float>>();
+      s->d_levels32[l]->ensure(static_cast<size_t>(n));
+      cuda_check(ermc_dev::launch_to_fp32(s->d_levels[l]->p, s->d_levels32[l]->p, n, st),
+                 "to_fp32");
+      ++s->launches;
+    }
+    P.lv[l].field32 = s->d_levels32[l]->p;
+  }
+  P.iv32 = s->d_iv32.p;
+  P.inv_dt32 = static_cast<float>(1.0 / v.dt);
+  P.t0_32 = static_cast<float>(v.t0);
+}
+
+template <typename F>
+int guarded(char* errbuf, size_t errlen, F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(errbuf, errlen, e.what());
+    return 1;
+  } catch (...) {
+    put_err(errbuf, errlen, "ermc_b200: unknown error");
+    return 1;
+  }
+}
+
+// Pinned staging for the host-buffer entry points (H2D of T, D2H of Q_r).
+int solve_host(const ermc_grid_t* grid, const double* temperature,
+               const ermc_boundary_t* boundary, const ermc_model_t* model,
+               const ermc_config_t* config, int64_t lo, int64_t hi,
+               ermc_solution_t* out, char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!out) throw Error("ermc_b200: null solution");
+    std::unique_ptr<ermc_session> s(create_session(grid, boundary, model, config));
+    DeviceGuard guard(s->device);
+    cudaStream_t st;
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    set_field_impl(s.get(), temperature, 0, st);
+    const int64_t n = hi - lo;
+    DevBuf<double> dq, dsd;
+    dq.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    dsd.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    session_solve_impl(s.get(), lo, hi, dq.p, dsd.p, out->steps_per_level, st);
+    if (n > 0) {
+      cuda_check(cudaMemcpyAsync(out->q_r, dq.p, n * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st), "D2H q_r");
+      cuda_check(cudaMemcpyAsync(out->std_dev, dsd.p, n * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st), "D2H std_dev");
+    }
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    int64_t total = 0;
+    for (int l = 0; l < config->n_levels; ++l) total += out->steps_per_level[l];
+    out->total_steps = total;
+    out->wall_time = std::chrono::duration<double>(
+                         std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+void ermc_b200_config_default(ermc_config_t* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->rays_per_cell = 2000;
+  c->n_levels = 1;
+  c->tolerance = 1e-4;
+  c->seed = 0;
+  c->max_steps = 100000;
+  c->sorting = 0;
+  c->steps_per_level = 5;
+  c->coarsen_ratio = 2;
+  c->volume_sampling = 0;
+  c->specular_walls = 0;
+  c->workers = 0;
+  c->precision = ERMC_PRECISION_FP64;
+  c->device = -1;
+}
+
+int ermc_b200_solve(const ermc_grid_t* grid, const double* temperature,
+                    const ermc_boundary_t* boundary, const ermc_model_t* model,
+                    const ermc_config_t* config, ermc_solution_t* out,
+                    char* errbuf, size_t errlen) {
+  const int64_t n = grid ? cells_of(*grid) : 0;
+  return solve_host(grid, temperature, boundary, model, config, 0, n, out,
+                    errbuf, errlen);
+}
+
+int ermc_b200_solve_range(const ermc_grid_t* grid, const double* temperature,
+                          const ermc_boundary_t* boundary,
+                          const ermc_model_t* model,
+                          const ermc_config_t* config, int64_t cell_lo,
+                          int64_t cell_hi, ermc_solution_t* out, char* errbuf,
+                          size_t errlen) {
+  return solve_host(grid, temperature, boundary, model, config, cell_lo,
+                    cell_hi, out, errbuf, errlen);
+}
+
+ermc_session_t* ermc_b200_session_create(const ermc_grid_t* grid,
+                                         const ermc_boundary_t* boundary,
+                                         const ermc_model_t* model,
+                                         const ermc_config_t* config,
+                                         char* errbuf, size_t errlen) {
+  ermc_session* s = nullptr;
+  guarded(errbuf, errlen, [&] { s = create_session(grid, boundary, model, config); });
+  return s;
+}
+
+void ermc_b200_session_destroy(ermc_session_t* s) {
+  if (!s) return;
+  {
+    DeviceGuard guard(s->device);
+    delete s;
+  }
+}
+
+int ermc_b200_session_set_field(ermc_session_t* s, const double* temperature,
+                                int is_device, void* stream, char* errbuf,
+                                size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    if (!s || !temperature) throw Error("ermc_b200: null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
+    set_field_impl(s, temperature, is_device, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ermc_b200_session_solve(ermc_session_t* s, int64_t cell_lo,
+                            int64_t cell_hi, double* d_q_r, double* d_std_dev,
+                            int64_t* steps_per_level, void* stream,
+                            char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    if (!s || !steps_per_level) throw Error("ermc_b200: null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
+    session_solve_impl(s, cell_lo, cell_hi, d_q_r, d_std_dev, steps_per_level,
+                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ermc_b200_session_timings(const ermc_session_t* s, double* ms4,
+                              int32_t* n_launches) {
+  if (!s) return 1;
+  for (int i = 0; i < 4; ++i) ms4[i] = s->ms[i];
+  if (n_launches) *n_launches = s->launches;
+  return 0;
+}
+
+int ermc_b200_trace_rays(const ermc_grid_t* grid, const double* temperature,
+                         const ermc_boundary_t* boundary,
+                         const ermc_model_t* model, const ermc_config_t* config,
+                         double t_max, double q_emission, int64_t n,
+                         const int64_t* cell_ids, const uint32_t* ray_ids,
+                         const double* dir_override, ermc_ray_result_t* out,
+                         int64_t* level_steps, char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    std::unique_ptr<ermc_session> s(create_session(grid, boundary, model, config));
+    DeviceGuard guard(s->device);
+    cudaStream_t st = nullptr;
+    set_field_impl(s.get(), temperature, 0, st);
+    Prepared pr;
+    prepare(s.get(), pr, t_max, q_emission, true, st);
+    DevBuf<int64_t> dc;
+    DevBuf<uint32_t> dr;
+    DevBuf<double> dd;
+    DevBuf<ermc_dev::RayRecord> drec;
+    DevBuf<int64_t> dls;
+    dc.upload(cell_ids, n, st);
+    dr.upload(ray_ids, n, st);
+    if (dir_override) dd.upload(dir_override, 3 * n, st);
+    drec.ensure(n);
+    if (level_steps) dls.ensure(static_cast<size_t>(n) * config->n_levels);
+    cuda_check(ermc_dev::launch_trace_rays_fp64(pr.P, n, dc.p, dr.p,
+                                                dir_override ? dd.p : nullptr,
+                                                drec.p, level_steps ? dls.p : nullptr, st),
+               "trace_rays");
+    std::vector<ermc_dev::RayRecord> recs(n);
+    cuda_check(cudaMemcpy(recs.data(), drec.p, n * sizeof(ermc_dev::RayRecord),
+                          cudaMemcpyDeviceToHost), "D2H");
+    if (level_steps)
+      cuda_check(cudaMemcpy(level_steps, dls.p, n * config->n_levels * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t i = 0; i < n; ++i) {
+      const ermc_dev::RayRecord& r = recs[i];
+      if (r.err != ermc_dev::kErrNone)
+        throw Error(error_message(s.get(), r, cell_ids[i], ray_ids[i]));
+      ermc_ray_result_t& o = out[i];
+      std::memset(&o, 0, sizeof(o));
+      o.q_contribution = r.q;
+      o.weight_absorbed = r.w_abs;
+      o.weight_walls = r.w_walls;
+      o.weight_residual = r.w_res;
+      for (int a = 0; a < 3; ++a) o.dir[a] = r.dir[a];
+      o.prefactor = r.prefactor;
+      o.ib_source = r.ib_source;
+      o.steps = r.steps;
+      o.terminated_by = r.term;
+      o.reflections = r.reflections;
+      o.band = r.band;
+      o.quad = r.quad;
+      o.next_draw = r.next_draw;
+    }
+  });
+}
+
+int ermc_b200_build_cdfs(const ermc_model_t* model, double t_max,
+                         double* band_cdf, double* quad_cdf, char* errbuf,
+                         size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    ermc_host::TableView v = ermc_host::make_view(*model);
+    ermc_host::build_cdfs(v, t_max, band_cdf, quad_cdf);
+  });
+}
+
+int ermc_b200_planck_mean(const ermc_model_t* model, double temperature,
+                          double* out, char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    ermc_host::TableView v = ermc_host::make_view(*model);
+    *out = ermc_host::planck_mean(v, temperature);
+  });
+}
+
+int ermc_b200_uniform_device(uint64_t seed, int64_t n, const uint64_t* cell_ids,
+                             const uint32_t* ray_ids, const uint32_t* draw_ids,
+                             double* out, char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+      cudaGetLastError();
+      throw Error("ermc_b200: no CUDA device available (the solver has no CPU path)");
+    }
+    cudaStream_t st = nullptr;
+    DevBuf<uint64_t> dc;
+    DevBuf<uint32_t> dr, dd;
+    DevBuf<double> dout;
+    dc.upload(cell_ids, n, st);
+    dr.upload(ray_ids, n, st);
+    dd.upload(draw_ids, n, st);
+    dout.ensure(n);
+    cuda_check(ermc_dev::launch_uniform(mix64_host(seed + 0x9e3779b97f4a7c15ULL), n,
+                                        dc.p, dr.p, dd.p, dout.p, st),
+               "uniform");
+    cuda_check(cudaMemcpy(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost),
+               "D2H");
+  });
+}
+
+int ermc_b200_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int ermc_b200_abi_version(void) { return ERMC_B200_ABI_VERSION; }
+
+}  // extern "C"

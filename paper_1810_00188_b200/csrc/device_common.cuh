@@ -1,0 +1,217 @@
+// device_common.cuh — pieces shared by the fp64 and fp32 trace kernels:
+// the keyed RNG, CDF inversion, cell decode and the persistent ray-pool
+// scheduler (the paper's persistent ray pool).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "trace_common.cuh"
+
+namespace ermc_dev {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+constexpr double kPiDev = 3.14159265358979323846;
+
+enum StepStatus : int { kContinue = 0, kDone = 1, kFail = 2 };
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  // MurmurHash3 fmix64 finaliser (reference sampling.cpp:13-20).
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+// uniform(RandomKey) with the seed and cell hashes hoisted out of the draw
+// (reference sampling.cpp:24-29): h_cell = mix64(mix64(seed + phi) ^ cell).
+__device__ __forceinline__ double draw_u(uint64_t h_cell, uint32_t ray,
+                                         uint32_t draw) {
+  const uint64_t h =
+      mix64(h_cell ^ ((static_cast<uint64_t>(ray) << 32) | draw));
+  return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+
+// std::upper_bound over a short ascending array (sampling.cpp:44-51).
+__device__ __forceinline__ int upper_bound_d(const double* a, int n, double x) {
+  int first = 0, count = n;
+  while (count > 0) {
+    const int step = count >> 1;
+    const int it = first + step;
+    if (!(x < __ldg(a + it))) {
+      first = it + 1;
+      count -= step + 1;
+    } else {
+      count = step;
+    }
+  }
+  return first;
+}
+
+// sample_band (reference sampling.cpp:42-53).
+__device__ __forceinline__ void sample_band(const TraceParams& P, double r_n,
+                                            double r_g, int& n, int& g) {
+  n = upper_bound_d(P.band_cdf, P.n_bands, r_n);
+  if (n >= P.n_bands) n = P.n_bands - 1;
+  g = upper_bound_d(P.quad_cdf + static_cast<int64_t>(n) * P.n_quad, P.n_quad,
+                    r_g);
+  if (g >= P.n_quad) g = P.n_quad - 1;
+}
+
+// Linear k-fastest index -> (i, j, k) (reference solver.cpp:120-122).
+__device__ __forceinline__ void decode_cell(const LevelDesc& L, int64_t cell,
+                                            int& ci, int& cj, int& ck) {
+  const int64_t nyz = static_cast<int64_t>(L.n[1]) * L.n[2];
+  if (cell < 0x7fffffffLL && nyz < 0x7fffffffLL) {
+    const uint32_t c = static_cast<uint32_t>(cell);
+    const uint32_t nz = static_cast<uint32_t>(L.n[2]);
+    ci = static_cast<int>(c / static_cast<uint32_t>(nyz));
+    cj = static_cast<int>((c / nz) % static_cast<uint32_t>(L.n[1]));
+    ck = static_cast<int>(c % nz);
+  } else {
+    ci = static_cast<int>(cell / nyz);
+    cj = static_cast<int>((cell / L.n[2]) % L.n[1]);
+    ck = static_cast<int>(cell % L.n[2]);
+  }
+}
+
+__device__ __forceinline__ void raise_error(const TraceParams& P, uint64_t key,
+                                            int code) {
+  const unsigned long long old =
+      atomicMin(P.err_key, static_cast<unsigned long long>(key + 1));
+  if (old == 0ull || old > key + 1) atomicExch(P.err_code, code);
+}
+
+// Persistent ray pool. Every lane owns one ray; when at least
+// refill_threshold lanes of a warp are idle they take the next work items
+// (cell-major (cell, ray) ids) from a warp-local pool, refilled with one
+// atomic per `kBatch` items from the chunk's global queue. Terminated rays
+// write their q to q_ray[ray][cell]; the per-cell reduction runs later in
+// ray-id order, so the schedule never changes a bit of the result.
+//
+// Tracer interface:
+//   int init(const TraceParams&, int64_t cell, uint32_t ray)  -> DevError
+//   int step(const TraceParams&, int max_steps)               -> StepStatus
+//   double finish(const TraceParams&)       residual dump, final q
+//   int err;  int level();  int sal();  int steps();
+template <class Tracer, bool kMulti>
+__device__ __forceinline__ void run_pool(const TraceParams& P,
+                                         unsigned long long* s_steps) {
+  constexpr uint64_t kBatch = 128;
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint32_t rays = static_cast<uint32_t>(P.rays);
+  const uint64_t n_work = P.n_work;
+  const int max_steps = static_cast<int>(
+      P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL);
+
+  Tracer tr;
+  bool active = false;
+  uint32_t slot_cell = 0, slot_ray = 0;
+  uint64_t my_work = 0;
+  uint64_t pool_next = 0, pool_end = 0;
+  bool exhausted = false;
+  unsigned long long my_steps = 0;
+
+  while (true) {
+    const unsigned idle = __ballot_sync(kFullMask, !active);
+    const int n_idle = __popc(idle);
+    const bool can_get = pool_next < pool_end || !exhausted;
+    if (can_get && (n_idle >= P.refill_threshold || idle == kFullMask)) {
+      const uint64_t avail = pool_end - pool_next;
+      uint64_t nb = 0, nb_end = 0;
+      if (avail < static_cast<uint64_t>(n_idle) && !exhausted) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(P.work_counter, kBatch);
+        b = __shfl_sync(kFullMask, b, 0);
+        if (b >= n_work) {
+          exhausted = true;
+        } else {
+          nb = b;
+          nb_end = b + kBatch < n_work ? b + kBatch : n_work;
+        }
+      }
+      if (!active) {
+        const uint64_t rank = __popc(idle & lt_mask);
+        uint64_t w = ~0ull;
+        if (rank < avail)
+          w = pool_next + rank;
+        else if (rank - avail < nb_end - nb)
+          w = nb + (rank - avail);
+        if (w != ~0ull) {
+          const uint32_t w32 = static_cast<uint32_t>(w);
+          slot_cell = w32 / rays;
+          slot_ray = w32 - slot_cell * rays;
+          my_work = w;
+          const int e = tr.init(P, P.cell_base + slot_cell, slot_ray);
+          if (e == kErrNone)
+            active = true;
+          else
+            raise_error(P, w, e);
+        }
+      }
+      if (avail >= static_cast<uint64_t>(n_idle)) {
+        pool_next += n_idle;
+      } else if (nb_end > nb) {
+        uint64_t take = n_idle - avail;
+        if (take > nb_end - nb) take = nb_end - nb;
+        pool_next = nb + take;
+        pool_end = nb_end;
+      } else {
+        pool_next = pool_end;
+      }
+    }
+    if (__ballot_sync(kFullMask, active) == 0u && exhausted &&
+        pool_next >= pool_end)
+      break;
+    if (active) {
+      const int st = tr.step(P, max_steps);
+      if (st != kContinue) {
+        active = false;
+        if (st == kDone) {
+          const double q = tr.finish(P);
+          if (isfinite(q) && tr.finite_state()) {
+            P.q_ray[static_cast<uint64_t>(slot_ray) * P.n_cells + slot_cell] = q;
+            if (kMulti) {
+              for (int l = 0; l < tr.level(); ++l)
+                atomicAdd(&s_steps[l],
+                          static_cast<unsigned long long>(P.lv[l].cap));
+              atomicAdd(&s_steps[tr.level()],
+                        static_cast<unsigned long long>(tr.sal()));
+            } else {
+              my_steps += static_cast<unsigned long long>(tr.steps());
+            }
+          } else {
+            raise_error(P, my_work, kErrNonFinite);
+          }
+        } else {
+          raise_error(P, my_work, tr.err);
+        }
+      }
+    }
+  }
+  if (!kMulti) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      my_steps += __shfl_xor_sync(kFullMask, my_steps, o);
+    if (lane == 0) atomicAdd(&s_steps[0], my_steps);
+  }
+}
+
+// Common kernel prologue/epilogue around run_pool.
+template <class Tracer, bool kMulti>
+__device__ __forceinline__ void pool_kernel_body(const TraceParams& P) {
+  __shared__ unsigned long long s_steps[kMaxLevels];
+  if (threadIdx.x < kMaxLevels) s_steps[threadIdx.x] = 0ull;
+  __syncthreads();
+  run_pool<Tracer, kMulti>(P, s_steps);
+  __syncthreads();
+  if (threadIdx.x < static_cast<unsigned>(P.n_levels) &&
+      s_steps[threadIdx.x] != 0ull)
+    atomicAdd(P.steps_per_level + threadIdx.x, s_steps[threadIdx.x]);
+}
+
+}  // namespace ermc_dev

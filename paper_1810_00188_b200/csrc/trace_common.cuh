@@ -1,0 +1,100 @@
+// trace_common.cuh — parameter blocks shared by the host launcher
+// (capi.cu) and the trace kernels (trace_fp64.cu, trace_fp32.cu).
+//
+// Everything the kernel needs is precomputed on the host with the reference's
+// own arithmetic (bitwise): per-level grid constants, T_max-derived sampling
+// CDFs, k(n,g,T_max) and Ib(n,T_max), wall blackbodies per (face, band),
+// the emission weight QE and the seed hash. The kernel then only marches.
+#pragma once
+
+#include <cstdint>
+
+namespace ermc_dev {
+
+constexpr int kMaxLevels = 16;
+
+// One multigrid level (reference GridHierarchy, geometry.hpp:74-83).
+struct LevelDesc {
+  int32_t n[3];      // cells per axis
+  int32_t cap;       // steps before demotion; -1 = uncapped (coarsest level)
+  double d[3];       // spacing per axis
+  double origin[3];  // grid origin
+  double extent[3];  // n * d, computed as CartesianGrid::extent
+  double eps;        // geom_eps = 1e-12 * min spacing (geometry.hpp:114-116)
+  const double* field;   // fp64 temperature, k-fastest
+  const float* field32;  // fp32 copy for the fast kernel (may be null)
+};
+
+// Error codes raised on the device; the host re-traces the failing ray
+// through the debug kernel to build the reference's message.
+enum DevError : int32_t {
+  kErrNone = 0,
+  kErrNonFinite = 1,      // tracer.cpp:134-138
+  kErrTableRange = 2,     // spectral.cpp:149-153
+  kErrTransparent = 3,    // sampling.cpp:91-93
+  kErrLocate = 4,         // geometry.cpp:119-127
+};
+
+struct TraceParams {
+  // ---- geometry ----
+  int32_t n_levels;
+  int32_t periodic[3];
+  LevelDesc lv[kMaxLevels];
+  double wall_eps[6];        // face = 2*axis + (hi ? 1 : 0)
+  const double* wall_ib;     // [6][n_bands] interp_ib(band, T_wall) or 0
+
+  // ---- spectral tables ----
+  int32_t n_bands, n_quad, n_temps;
+  int32_t uniform_temps;     // SpectralModel uniform fast path (spectral.cpp:119-129)
+  double t0, dt;             // uniform grid origin and step
+  const double* temps;       // [n_temps]
+  const double* k;           // [n_bands][n_quad][n_temps]
+  const double* ib;          // [n_bands][n_temps]
+  const double* band_cdf;    // [n_bands]
+  const double* quad_cdf;    // [n_bands][n_quad]
+  const double* k_max;       // [n_bands][n_quad]  k(n,g,T_max)
+  const double* ib_max;      // [n_bands]          Ib(n,T_max)
+
+  // ---- fp32 fast-path tables (trace_fp32.cu) ----
+  const float4* iv32;        // [n_bands*n_quad][n_temps-1] {k_lo, k_hi-k_lo, ib_lo, ib_hi-ib_lo}
+  const float* wall_ibn32;   // [6][n_bands] wall Ib / Ib(n, T_last)
+  float inv_dt32;            // 1/dt for the fp32 lookup (uniform grids only)
+  float t0_32;
+
+  // ---- march options (TraceOptions, tracer.hpp:26-30) ----
+  double qe;                 // 4 kappa_p(T_max) sigma T_max^4 / R (solver.cpp:92-93)
+  double tol;
+  int64_t max_steps;
+  int32_t specular;
+  int32_t volume_sampling;
+  uint64_t h_seed;           // mix64(seed + 0x9e3779b97f4a7c15) (sampling.cpp:25)
+  int32_t rays;              // rays per cell
+
+  // ---- work decomposition ----
+  int32_t refill_threshold;  // idle lanes before a warp regenerates rays
+  int64_t cell_base;         // first global linear cell of this chunk
+  int64_t n_cells;           // cells in this chunk
+  uint64_t n_work;           // n_cells * rays (ray work items)
+  unsigned long long* work_counter;
+  double* q_ray;             // [rays][n_cells] per-ray q contributions
+  unsigned long long* steps_per_level;  // [n_levels]
+  unsigned long long* err_key;          // min failing work item + 1 (0 = none)
+  int32_t* err_code;
+};
+
+// Debug / test record of one traced ray (ermc_ray_result_t mirror).
+struct RayRecord {
+  double q;
+  double w_abs, w_walls, w_res;
+  double dir[3];
+  double prefactor, ib_source;
+  int64_t steps;
+  int32_t term, reflections, band, quad;
+  uint32_t next_draw;
+  int32_t err;
+  double err_value;   // offending temperature / coordinate
+  int32_t err_axis;
+  int32_t pad;
+};
+
+}  // namespace ermc_dev

@@ -1,0 +1,386 @@
+// trace_fp32.cu — fast variant of the ERMC trace kernel (precision = fp32).
+//
+// Same work decomposition, RNG keys and (band, g) sampling as the fp64
+// kernel (every ray is the reference's ray: the draws and the CDF
+// inversion stay exact), but the march runs in fp32 with a layout built
+// for the gather roofline:
+//   * T as fp32 (64 MiB at 256^3: L2-resident on a 126 MB L2);
+//   * one 16-byte float4 per (band, g, T-interval):
+//       {k_lo, k_hi - k_lo, ibn_lo, ibn_hi - ibn_lo},  ibn = Ib / Ib(T_last)
+//     so a step is one 4-byte T gather + one 16-byte table load (the 20 B/step
+//     of BASELINE.md's roofline);
+//   * Amanatides-Woo in absolute ray parameters (one add per step), with
+//     the running position re-based at wraps/reflections;
+//   * the reciprocal exchange accumulated as tau*alpha*(ibn2 - ibn1) and
+//     scaled once per ray by QE * k1/k_max * Ib(T_last)/Ib_max (in fp64).
+// Parity contract: statistical — per cell within 3 sigma of the fp64 path
+// (north_star), total steps within 1e-3.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "trace_common.cuh"
+
+namespace ermc_dev {
+
+namespace {
+
+constexpr int kBlock32 = 128;
+
+// 1 - exp(-x) for x >= 0: Taylor near 0 (no cancellation), ex2 otherwise.
+__device__ __forceinline__ float absorb32(float x) {
+  if (x < 0.125f) {
+    float p = fmaf(x, -1.0f / 120.0f, 1.0f / 24.0f);
+    p = fmaf(x, -p, 1.0f / 6.0f);
+    p = fmaf(x, -p, 0.5f);
+    p = fmaf(x, -p, 1.0f);
+    return x * p;
+  }
+  return 1.0f - __expf(-x);
+}
+
+struct Fp32Tracer {
+  float p0[3];   // position at s = 0
+  float dir[3];
+  float tn[3];   // absolute ray parameter of the next face on each axis
+  float td[3];
+  float s;       // current ray parameter
+  float tau, acc, ib1n, last_ib2n;
+  double cq;     // QE * k1/k_max * Ib(T_last)/Ib_max  (per ray)
+  const float4* row;
+  int idx[3], stp[3];
+  int dlin[3];   // signed linear stride of one step on each axis
+  int lin;
+  int band, lvl, sal_, steps_;
+  uint32_t next_draw, ray_id;
+  uint64_t h_cell;
+  int err;
+
+  __device__ __forceinline__ void setup(const LevelDesc& L) {
+    const int stride[3] = {L.n[1] * L.n[2], L.n[2], 1};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float da = dir[a];
+      if (da == 0.0f) {
+        tn[a] = __int_as_float(0x7f800000);
+        td[a] = __int_as_float(0x7f800000);
+        stp[a] = 0;
+        dlin[a] = 0;
+        continue;
+      }
+      const float inv = 1.0f / da;
+      stp[a] = da > 0.0f ? 1 : -1;
+      dlin[a] = da > 0.0f ? stride[a] : -stride[a];
+      const float face = static_cast<float>(
+          L.origin[a] + (idx[a] + (da > 0.0f ? 1 : 0)) * L.d[a]);
+      tn[a] = (face - p0[a]) * inv;
+      td[a] = static_cast<float>(L.d[a]) * fabsf(inv);
+    }
+    s = 0.0f;
+    lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
+  }
+
+  // Position at the current parameter; re-base so s = 0.
+  __device__ __forceinline__ void rebase() {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      p0[a] = fmaf(s, dir[a], p0[a]);
+      tn[a] -= s;
+    }
+    s = 0.0f;
+  }
+
+  __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
+                                      uint32_t ray) {
+    const LevelDesc& L = P.lv[0];
+    int ci, cj, ck;
+    decode_cell(L, cell, ci, cj, ck);
+    h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(cell));
+    ray_id = ray;
+    const double r_theta = draw_u(h_cell, ray, 0);
+    const double r_phi = draw_u(h_cell, ray, 1);
+    const double r_n = draw_u(h_cell, ray, 2);
+    const double r_g = draw_u(h_cell, ray, 3);
+    next_draw = 4;
+    const float cos_t = static_cast<float>(1.0 - 2.0 * r_theta);
+    const float sin_t = sqrtf(fmaxf(0.0f, 1.0f - cos_t * cos_t));
+    float sp, cp;
+    sincospif(static_cast<float>(2.0 * r_phi), &sp, &cp);
+    dir[0] = sin_t * cp;
+    dir[1] = sin_t * sp;
+    dir[2] = cos_t;
+    int n, g;
+    sample_band(P, r_n, r_g, n, g);
+    band = n;
+    const int nt1 = P.n_temps - 1;
+    row = P.iv32 + (static_cast<int64_t>(n) * P.n_quad + g) * nt1;
+    idx[0] = ci;
+    idx[1] = cj;
+    idx[2] = ck;
+    double pos[3] = {L.origin[0] + (ci + 0.5) * L.d[0],
+                     L.origin[1] + (cj + 0.5) * L.d[1],
+                     L.origin[2] + (ck + 0.5) * L.d[2]};
+    if (P.volume_sampling) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        pos[a] += (draw_u(h_cell, ray, next_draw++) - 0.5) * L.d[a];
+    }
+    p0[0] = static_cast<float>(pos[0]);
+    p0[1] = static_cast<float>(pos[1]);
+    p0[2] = static_cast<float>(pos[2]);
+    const float t_cell = __ldg(L.field32 + cell);
+    float u = fmaf(t_cell, P.inv_dt32, -P.t0_32 * P.inv_dt32);
+    int lo = min(max(static_cast<int>(u), 0), nt1 - 1);
+    const float f = u - static_cast<float>(lo);
+    const float4 v = __ldg(row + lo);
+    const float k1 = fmaf(f, v.y, v.x);
+    ib1n = fmaf(f, v.w, v.z);
+    last_ib2n = ib1n;
+    const double kmax = __ldg(P.k_max + static_cast<int64_t>(n) * P.n_quad + g);
+    const double ibmax = __ldg(P.ib_max + n);
+    if (kmax <= 0.0 || ibmax <= 0.0) return kErrTransparent;
+    // R_I / Ib1 * QE with Ib normalised by Ib(T_last): see file header.
+    const double ib_last = __ldg(P.ib + static_cast<int64_t>(n) * P.n_temps + nt1);
+    cq = P.qe * static_cast<double>(k1) / kmax * (ib_last / ibmax);
+    tau = 1.0f;
+    acc = 0.0f;
+    lvl = 0;
+    sal_ = 0;
+    steps_ = 0;
+    setup(L);
+    return kErrNone;
+  }
+
+  template <bool kMulti>
+  __device__ __forceinline__ int step_t(const TraceParams& P, int max_steps) {
+    if (tau <= static_cast<float>(P.tol)) return kDone;
+    if (steps_ >= max_steps) return kDone;
+    if (kMulti) {
+      const int cap = P.lv[lvl].cap;
+      if (cap >= 0 && sal_ >= cap && lvl + 1 < P.n_levels) {
+        ++lvl;
+        const LevelDesc& C = P.lv[lvl];
+        rebase();
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float p = fmaf(static_cast<float>(C.eps), dir[a], p0[a]);
+          const float rel = (p - static_cast<float>(C.origin[a])) /
+                            static_cast<float>(C.d[a]);
+          int i = static_cast<int>(floorf(rel));
+          i = min(max(i, 0), C.n[a] - 1);
+          idx[a] = i;
+        }
+        sal_ = 0;
+        setup(C);
+      }
+    }
+    const LevelDesc& L = P.lv[kMulti ? lvl : 0];
+    int axis = 0;
+    float tmin = tn[0];
+    if (tn[1] < tmin) {
+      tmin = tn[1];
+      axis = 1;
+    }
+    if (tn[2] < tmin) {
+      tmin = tn[2];
+      axis = 2;
+    }
+    const float ds = fmaxf(tmin - s, 0.0f);
+    s = fmaxf(tmin, s);
+
+    const float t_cell = __ldg(L.field32 + lin);
+    const float u = fmaf(t_cell, P.inv_dt32, -P.t0_32 * P.inv_dt32);
+    const int lo = min(max(static_cast<int>(u), 0), P.n_temps - 2);
+    const float f = u - static_cast<float>(lo);
+    const float4 v = __ldg(row + lo);
+    const float kappa = fmaf(f, v.y, v.x);
+    const float ib2n = fmaf(f, v.w, v.z);
+    const float alpha = absorb32(kappa * ds);
+    last_ib2n = ib2n;
+    const float ta = tau * alpha;
+    acc = fmaf(ta, ib2n - ib1n, acc);
+    tau -= ta;
+
+    int ia = 0, na = 0, sa = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) {
+        tn[a] += td[a];
+        idx[a] += stp[a];
+        lin += dlin[a];
+        ia = idx[a];
+        na = L.n[a];
+        sa = stp[a];
+      }
+    ++steps_;
+    if (kMulti) ++sal_;
+    if (ia >= 0 && ia < na) return kContinue;
+
+    if (P.periodic[axis]) {
+      rebase();
+      const float ext = static_cast<float>(L.extent[axis]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) {
+          if (ia < 0) {
+            idx[a] = na - 1;
+            p0[a] += ext;
+          } else {
+            idx[a] = 0;
+            p0[a] -= ext;
+          }
+        }
+      lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
+      return kContinue;
+    }
+
+    // wall exchange (tracer.cpp:155-165)
+    const bool at_hi = sa > 0;
+    const int face = 2 * axis + (at_hi ? 1 : 0);
+    const float ew = static_cast<float>(P.wall_eps[face]);
+    const float ibw = __ldg(P.wall_ibn32 + face * P.n_bands + band);
+    const float tw = tau * ew;
+    acc = fmaf(tw, ibw - ib1n, acc);
+    tau -= tw;
+    if (tau <= static_cast<float>(P.tol)) return kDone;
+    // reflection (tracer.cpp:167-182)
+    rebase();
+    const float face_pos = static_cast<float>(
+        L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
+    float nd[3] = {dir[0], dir[1], dir[2]};
+    if (P.specular) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) nd[a] = -nd[a];
+    } else {
+      const double r1 = draw_u(h_cell, ray_id, next_draw++);
+      const double r2 = draw_u(h_cell, ray_id, next_draw++);
+      const float sin_t = sqrtf(static_cast<float>(r1));
+      const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
+      float sp, cp;
+      sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
+      const int t1 = axis == 2 ? 0 : axis + 1;
+      const int t2 = axis == 0 ? 2 : axis - 1;
+      const float inward = at_hi ? -1.0f : 1.0f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a == axis) nd[a] = inward * cos_t;
+        if (a == t1) nd[a] = sin_t * cp;
+        if (a == t2) nd[a] = sin_t * sp;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a == axis) {
+        idx[a] -= stp[a];
+        p0[a] = face_pos;
+      }
+      dir[a] = nd[a];
+    }
+    setup(L);
+    return kContinue;
+  }
+
+  __device__ __forceinline__ double finish(const TraceParams&) const {
+    const float a = fmaf(tau, last_ib2n - ib1n, acc);
+    return cq * static_cast<double>(a);
+  }
+  __device__ __forceinline__ bool finite_state() const {
+    return isfinite(tau) && isfinite(acc);
+  }
+  __device__ __forceinline__ int level() const { return lvl; }
+  __device__ __forceinline__ int sal() const { return sal_; }
+  __device__ __forceinline__ int steps() const { return steps_; }
+};
+
+struct Fp32Single : Fp32Tracer {
+  __device__ __forceinline__ int step(const TraceParams& P, int m) {
+    return step_t<false>(P, m);
+  }
+};
+struct Fp32Multi : Fp32Tracer {
+  __device__ __forceinline__ int step(const TraceParams& P, int m) {
+    return step_t<true>(P, m);
+  }
+};
+
+template <bool kMulti>
+__global__ void __launch_bounds__(kBlock32, 6)
+    trace_pool_fp32(const __grid_constant__ TraceParams P) {
+  if (kMulti)
+    pool_kernel_body<Fp32Multi, true>(P);
+  else
+    pool_kernel_body<Fp32Single, false>(P);
+}
+
+// {k_lo, k_hi - k_lo, ibn_lo, ibn_hi - ibn_lo} per (band, g, interval),
+// ibn = Ib / Ib(n, T_last).
+__global__ void build_iv32(const double* __restrict__ k,
+                           const double* __restrict__ ib, int nb, int nq,
+                           int nt, float4* __restrict__ iv) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t n_iv = static_cast<int64_t>(nb) * nq * (nt - 1);
+  if (i >= n_iv) return;
+  const int t = static_cast<int>(i % (nt - 1));
+  const int64_t ng = i / (nt - 1);
+  const int n = static_cast<int>(ng / nq);
+  const double* krow = k + ng * nt;
+  const double* ibrow = ib + static_cast<int64_t>(n) * nt;
+  const double ilast = ibrow[nt - 1];
+  const double s = ilast > 0.0 ? 1.0 / ilast : 0.0;
+  const double b0 = ibrow[t] * s, b1 = ibrow[t + 1] * s;
+  iv[i] = make_float4(static_cast<float>(krow[t]),
+                      static_cast<float>(krow[t + 1] - krow[t]),
+                      static_cast<float>(b0), static_cast<float>(b1 - b0));
+}
+
+__global__ void to_fp32(const double* __restrict__ src, float* __restrict__ dst,
+                        int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<float>(src[i]);
+}
+
+}  // namespace
+
+int trace_fp32_block() { return kBlock32; }
+
+int trace_fp32_blocks_per_sm(bool multi) {
+  int nb = 0;
+  if (multi)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp32<true>,
+                                                  kBlock32, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp32<false>,
+                                                  kBlock32, 0);
+  return nb;
+}
+
+cudaError_t launch_trace_fp32(const TraceParams& P, int grid,
+                              cudaStream_t stream) {
+  if (P.n_levels > 1)
+    trace_pool_fp32<true><<<grid, kBlock32, 0, stream>>>(P);
+  else
+    trace_pool_fp32<false><<<grid, kBlock32, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_iv32(const double* k, const double* ib, int nb, int nq,
+                              int nt, float4* iv, cudaStream_t stream) {
+  const int64_t n = static_cast<int64_t>(nb) * nq * (nt - 1);
+  if (n <= 0) return cudaSuccess;
+  build_iv32<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+      k, ib, nb, nq, nt, iv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_fp32(const double* src, float* dst, int64_t n,
+                           cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  to_fp32<<<1184, 256, 0, stream>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
+}  // namespace ermc_dev

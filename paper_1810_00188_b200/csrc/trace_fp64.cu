@@ -1,0 +1,678 @@
+// trace_fp64.cu — the ERMC hot path on sm_100a, reference (fp64) arithmetic.
+//
+// K1 `trace_pool_fp64`: fused init_ray + march for every (cell, ray) work
+// item of a cell range (reference sampling.cpp:55-96, tracer.cpp:57-194,
+// driven per cell by solver.cpp:115-140). One persistent CTA set covers the
+// SMs; every lane owns one ray at a time and regenerates a new ray from a
+// warp-local work pool when its ray terminates (the paper's persistent ray
+// pool), so lanes never wait for the longest ray of a
+// batch. The per-ray reciprocal exchange q is written to q_ray[ray][cell];
+// K2 `reduce_cells` then does the reference's per-cell sum + Welford in
+// ray-id order (solver.cpp:142-155), so results do not depend on the
+// marching order — the GPU analogue of the reference's worker/sorting
+// invariance (P5, P8).
+//
+// This translation unit is compiled with --fmad=false and IEEE div/sqrt so
+// every add/mul/div rounds exactly like the reference's x86-64 build (no FMA
+// contraction). Only libdevice expm1/sin/cos may differ from glibc by an
+// ulp, which bounds the per-cell parity.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "trace_common.cuh"
+
+namespace ermc_dev {
+
+namespace {
+
+constexpr double kPiD = kPiDev;
+constexpr unsigned kFull = kFullMask;
+
+// SpectralModel::lookup (reference spectral.cpp:148-177). Returns false when
+// T is outside the table (the reference throws).
+__device__ __forceinline__ bool t_lookup(const TraceParams& P, double T,
+                                         int& lo, double& frac) {
+  const double* tg = P.temps;
+  const int nt = P.n_temps;
+  if (!(T >= __ldg(tg) && T <= __ldg(tg + nt - 1))) return false;
+  if (nt < 2) {  // single node: exact (the reference indexes node -1 here)
+    lo = 0;
+    frac = 0.0;
+    return true;
+  }
+  if (P.uniform_temps) {
+    int l = static_cast<int>((T - P.t0) / P.dt);
+    l = min(max(l, 0), nt - 2);
+    double a = __ldg(tg + l), b = __ldg(tg + l + 1);
+    double f = (T - a) / (b - a);
+    if (f < 0.0 && l > 0) {
+      --l;
+      f = (T - __ldg(tg + l)) / (__ldg(tg + l + 1) - __ldg(tg + l));
+    } else if (f > 1.0 && l < nt - 2) {
+      ++l;
+      f = (T - __ldg(tg + l)) / (__ldg(tg + l + 1) - __ldg(tg + l));
+    }
+    lo = l;
+    frac = f;
+    return true;
+  }
+  int hi = upper_bound_d(tg, nt, T);
+  if (hi == 0) {
+    lo = 0;
+    frac = 0.0;
+  } else if (hi == nt) {
+    lo = nt - 2;
+    frac = 1.0;
+  } else {
+    lo = hi - 1;
+    double a = __ldg(tg + lo);
+    frac = (T - a) / (__ldg(tg + hi) - a);
+  }
+  return true;
+}
+
+// a + frac*(b - a) with the frac == 0 exact shortcut (spectral.cpp:179-205).
+__device__ __forceinline__ double interp_row(const double* row, int lo,
+                                             double frac) {
+  double a = __ldg(row + lo);
+  if (frac == 0.0) return a;
+  return a + frac * (__ldg(row + lo + 1) - a);
+}
+
+struct Ray {
+  double pos[3], dir[3], tn[3], td[3];
+  double tau, q, last_ib2, ib1, pref;
+  const double* krow;
+  const double* ibrow;
+  int idx[3], stp[3];
+  int band, level, sal, steps;
+  uint32_t next_draw, ray_id;
+  uint64_t h_cell;
+};
+
+struct DebugRec {
+  double w_abs, w_walls;
+  int reflections, term;
+  int64_t level_steps[kMaxLevels];
+  double err_value;
+  int err_axis;
+};
+
+// Dda::setup (reference tracer.cpp:17-38).
+__device__ __forceinline__ void dda_setup(const LevelDesc& L, Ray& r) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double da = r.dir[a];
+    if (da == 0.0) {
+      r.tn[a] = __longlong_as_double(0x7ff0000000000000LL);
+      r.td[a] = __longlong_as_double(0x7ff0000000000000LL);
+      r.stp[a] = 0;
+      continue;
+    }
+    r.stp[a] = da > 0.0 ? 1 : -1;
+    int face_idx = r.idx[a] + (da > 0.0 ? 1 : 0);
+    double face = L.origin[a] + face_idx * L.d[a];
+    r.tn[a] = (face - r.pos[a]) / da;
+    r.td[a] = L.d[a] / fabs(da);
+  }
+}
+
+// init_ray (reference sampling.cpp:55-96) for global cell `cell`, with the
+// level-0 grid. Returns an error code (0 = ok).
+__device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
+                                        uint32_t ray_id, Ray& r,
+                                        const double* dir_override) {
+  const LevelDesc& L = P.lv[0];
+  int ci, cj, ck;
+  decode_cell(L, cell, ci, cj, ck);
+  r.h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(cell));
+  r.ray_id = ray_id;
+  double r_theta = draw_u(r.h_cell, ray_id, 0);
+  double r_phi = draw_u(r.h_cell, ray_id, 1);
+  double r_n = draw_u(r.h_cell, ray_id, 2);
+  double r_g = draw_u(r.h_cell, ray_id, 3);
+  r.next_draw = 4;
+
+  // sample_direction (sampling.cpp:31-40)
+  double cos_t = 1.0 - 2.0 * r_theta;
+  double phi = 2.0 * kPiD * r_phi;
+  double sin_t = sqrt(fmax(0.0, 1.0 - cos_t * cos_t));
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  r.dir[0] = sin_t * cp;
+  r.dir[1] = sin_t * sp;
+  r.dir[2] = cos_t;
+  if (dir_override) {
+    r.dir[0] = dir_override[0];
+    r.dir[1] = dir_override[1];
+    r.dir[2] = dir_override[2];
+  }
+
+  int n, g;
+  sample_band(P, r_n, r_g, n, g);
+  r.band = n;
+  r.krow = P.k + (static_cast<int64_t>(n) * P.n_quad + g) * P.n_temps;
+  r.ibrow = P.ib + static_cast<int64_t>(n) * P.n_temps;
+
+  // cell centre (geometry.hpp:28-31), optional volume sampling
+  r.idx[0] = ci;
+  r.idx[1] = cj;
+  r.idx[2] = ck;
+  r.pos[0] = L.origin[0] + (ci + 0.5) * L.d[0];
+  r.pos[1] = L.origin[1] + (cj + 0.5) * L.d[1];
+  r.pos[2] = L.origin[2] + (ck + 0.5) * L.d[2];
+  if (P.volume_sampling) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      r.pos[a] += (draw_u(r.h_cell, ray_id, r.next_draw++) - 0.5) * L.d[a];
+  }
+
+  double t_cell = __ldg(L.field + cell);
+  int lo;
+  double frac;
+  if (!t_lookup(P, t_cell, lo, frac)) return kErrTableRange;
+  r.ib1 = interp_row(r.ibrow, lo, frac);
+  double k_max = __ldg(P.k_max + static_cast<int64_t>(n) * P.n_quad + g);
+  double ib_max = __ldg(P.ib_max + n);
+  if (k_max <= 0.0 || ib_max <= 0.0) return kErrTransparent;
+  r.pref = interp_row(r.krow, lo, frac) * r.ib1 / (k_max * ib_max);
+
+  // march() prologue (tracer.cpp:62-77)
+  r.tau = 1.0;
+  r.q = 0.0;
+  r.last_ib2 = r.ib1;
+  r.level = 0;
+  r.sal = 0;
+  r.steps = 0;
+  dda_setup(L, r);
+  return kErrNone;
+}
+
+// One iteration of march's loop (reference tracer.cpp:82-185).
+// kMulti enables the multigrid demotion branch (tracer.cpp:91-101).
+template <bool kMulti, bool kDebug>
+__device__ __forceinline__ int march_step(const TraceParams& P, Ray& r,
+                                          int max_steps, DebugRec* dbg,
+                                          int* err) {
+  if (r.tau <= P.tol) {
+    if (kDebug) dbg->term = 0;
+    return kDone;
+  }
+  if (r.steps >= max_steps) {
+    if (kDebug) dbg->term = 2;
+    return kDone;
+  }
+  if (kMulti) {
+    const int cap = P.lv[r.level].cap;
+    if (cap >= 0 && r.sal >= cap && r.level + 1 < P.n_levels) {
+      // Demote: same position/direction/transmissivity on coarser cells;
+      // locate(grid, pos, dir) (geometry.cpp:112-138).
+      ++r.level;
+      const LevelDesc& C = P.lv[r.level];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double p = r.pos[a] + C.eps * r.dir[a];
+        double rel = (p - C.origin[a]) / C.d[a];
+        int i = static_cast<int>(floor(rel));
+        if (i < 0 || i >= C.n[a]) {
+          if (rel >= -1e-9 && i < 0) {
+            i = 0;
+          } else if (rel <= C.n[a] + 1e-9 && i >= C.n[a]) {
+            i = C.n[a] - 1;
+          } else {
+            if (kDebug) {
+              dbg->err_axis = a;
+              dbg->err_value = rel;
+            }
+            *err = kErrLocate;
+            return kFail;
+          }
+        }
+        r.idx[a] = i;
+      }
+      r.sal = 0;
+      dda_setup(C, r);
+    }
+  }
+  const LevelDesc& L = P.lv[kMulti ? r.level : 0];
+
+  int axis = 0;
+  double ds = r.tn[0];
+  if (r.tn[1] < ds) {
+    ds = r.tn[1];
+    axis = 1;
+  }
+  if (r.tn[2] < ds) {
+    ds = r.tn[2];
+    axis = 2;
+  }
+  if (ds < 0.0) ds = 0.0;
+
+  const int64_t lin =
+      (static_cast<int64_t>(r.idx[0]) * L.n[1] + r.idx[1]) * L.n[2] + r.idx[2];
+  const double t_cell = __ldg(L.field + lin);
+  int lo;
+  double frac;
+  if (!t_lookup(P, t_cell, lo, frac)) {
+    if (kDebug) dbg->err_value = t_cell;
+    *err = kErrTableRange;
+    return kFail;
+  }
+  const double kappa = interp_row(r.krow, lo, frac);
+  const double ib2 = interp_row(r.ibrow, lo, frac);
+  const double alpha = -expm1(-kappa * ds);
+  r.last_ib2 = ib2;
+  r.q += P.qe * r.tau * alpha * ((ib2 - r.ib1) / r.ib1) * r.pref;
+  if (kDebug) dbg->w_abs += r.tau * alpha;
+  r.tau *= 1.0 - alpha;
+
+  const double advance = ds + L.eps;
+  r.pos[0] += advance * r.dir[0];
+  r.pos[1] += advance * r.dir[1];
+  r.pos[2] += advance * r.dir[2];
+  r.tn[0] -= advance;
+  r.tn[1] -= advance;
+  r.tn[2] -= advance;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (a == axis) r.tn[a] += r.td[a];
+  ++r.steps;
+  if (kMulti) ++r.sal;
+  if (kDebug) ++dbg->level_steps[r.level];
+
+  // Non-finite values propagate to the end of the ray, where the pool
+  // checks them; the debug tracer checks every step like the reference.
+  if (kDebug && (!isfinite(r.q) || !isfinite(r.tau))) {
+    *err = kErrNonFinite;
+    return kFail;
+  }
+
+  int ia = 0, na = 0, sa = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (a == axis) {
+      r.idx[a] += r.stp[a];
+      ia = r.idx[a];
+      na = L.n[a];
+      sa = r.stp[a];
+    }
+  if (ia >= 0 && ia < na) return kContinue;
+
+  if (P.periodic[axis]) {
+    const double ext = L.extent[axis];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) {
+        if (ia < 0) {
+          r.idx[a] = na - 1;
+          r.pos[a] += ext;
+        } else {
+          r.idx[a] = 0;
+          r.pos[a] -= ext;
+        }
+      }
+    return kContinue;
+  }
+
+  // Wall exchange, then absorption or reflection (tracer.cpp:155-184).
+  const bool at_hi = sa > 0;
+  const int face = 2 * axis + (at_hi ? 1 : 0);
+  const double ew = P.wall_eps[face];
+  const double ib_w = __ldg(P.wall_ib + face * P.n_bands + r.band);
+  r.q += P.qe * r.tau * ew * ((ib_w - r.ib1) / r.ib1) * r.pref;
+  if (kDebug) dbg->w_walls += r.tau * ew;
+  r.tau *= 1.0 - ew;
+  if (r.tau <= P.tol) {
+    if (kDebug) dbg->term = 1;
+    return kDone;
+  }
+  if (kDebug) ++dbg->reflections;
+  const double face_pos = L.origin[axis] + (at_hi ? L.extent[axis] : 0.0);
+  const int inward = at_hi ? -1 : 1;
+  double nd[3] = {r.dir[0], r.dir[1], r.dir[2]};
+  if (P.specular) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) nd[a] = -nd[a];
+  } else {
+    // diffuse_reflection (tracer.cpp:42-53)
+    double r1 = draw_u(r.h_cell, r.ray_id, r.next_draw++);
+    double r2 = draw_u(r.h_cell, r.ray_id, r.next_draw++);
+    double sin_t = sqrt(r1);
+    double cos_t = sqrt(1.0 - r1);
+    double phi = 2.0 * kPiD * r2;
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    const int t1 = axis == 2 ? 0 : axis + 1;
+    const int t2 = axis == 0 ? 2 : axis - 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a == axis) nd[a] = inward * cos_t;
+      if (a == t1) nd[a] = sin_t * cp;
+      if (a == t2) nd[a] = sin_t * sp;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a == axis) {
+      r.idx[a] -= r.stp[a];
+      r.pos[a] = face_pos;
+    }
+    r.dir[a] = nd[a];
+  }
+  r.pos[0] += L.eps * r.dir[0];
+  r.pos[1] += L.eps * r.dir[1];
+  r.pos[2] += L.eps * r.dir[2];
+  dda_setup(L, r);
+  return kContinue;
+}
+
+// Residual dump into the source cell (tracer.cpp:186-188).
+__device__ __forceinline__ double finish_ray(const TraceParams& P,
+                                             const Ray& r) {
+  return r.q + P.qe * r.tau * ((r.last_ib2 - r.ib1) / r.ib1) * r.pref;
+}
+
+struct Fp64Tracer {
+  Ray r;
+  int err;
+  __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
+                                      uint32_t ray) {
+    return init_ray(P, cell, ray, r, nullptr);
+  }
+  template <bool kMulti>
+  __device__ __forceinline__ int step_t(const TraceParams& P, int max_steps) {
+    return march_step<kMulti, false>(P, r, max_steps, nullptr, &err);
+  }
+  __device__ __forceinline__ double finish(const TraceParams& P) const {
+    return finish_ray(P, r);
+  }
+  __device__ __forceinline__ bool finite_state() const {
+    return isfinite(r.tau);
+  }
+  __device__ __forceinline__ int level() const { return r.level; }
+  __device__ __forceinline__ int sal() const { return r.sal; }
+  __device__ __forceinline__ int steps() const { return r.steps; }
+};
+struct Fp64Single : Fp64Tracer {
+  __device__ __forceinline__ int step(const TraceParams& P, int m) {
+    return step_t<false>(P, m);
+  }
+};
+struct Fp64Multi : Fp64Tracer {
+  __device__ __forceinline__ int step(const TraceParams& P, int m) {
+    return step_t<true>(P, m);
+  }
+};
+
+constexpr int kBlock = 128;
+
+// K1: persistent ray-pool trace over the chunk's (cell, ray) work items.
+template <bool kMulti>
+__global__ void __launch_bounds__(kBlock, 4)
+    trace_pool_fp64(const __grid_constant__ TraceParams P) {
+  if (kMulti)
+    pool_kernel_body<Fp64Multi, true>(P);
+  else
+    pool_kernel_body<Fp64Single, false>(P);
+}
+
+// Debug/test kernel: one thread traces one explicit ray with full
+// bookkeeping (weights, termination, per-level steps).
+__global__ void trace_rays_fp64(const __grid_constant__ TraceParams P,
+                                int64_t n, const int64_t* cells,
+                                const uint32_t* ray_ids, const double* dirs,
+                                RayRecord* out, int64_t* level_steps) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= n) return;
+  Ray r;
+  DebugRec dbg;
+  dbg.w_abs = dbg.w_walls = 0.0;
+  dbg.reflections = 0;
+  dbg.term = 0;
+  dbg.err_value = 0.0;
+  dbg.err_axis = -1;
+  for (int l = 0; l < kMaxLevels; ++l) dbg.level_steps[l] = 0;
+  RayRecord rec;
+  rec.err = kErrNone;
+  rec.err_value = 0.0;
+  rec.err_axis = -1;
+  int e = init_ray(P, cells[s], ray_ids[s], r, dirs ? dirs + 3 * s : nullptr);
+  if (e != kErrNone) {
+    rec.err = e;
+    if (e == kErrTableRange) rec.err_value = __ldg(P.lv[0].field + cells[s]);
+    out[s] = rec;
+    return;
+  }
+  rec.dir[0] = r.dir[0];
+  rec.dir[1] = r.dir[1];
+  rec.dir[2] = r.dir[2];
+  rec.prefactor = r.pref;
+  rec.ib_source = r.ib1;
+  // The reference's RayState leaves init_ray with next_draw = 4 (7 with
+  // volume sampling); march consumes reflection draws on its own copy.
+  rec.next_draw = r.next_draw;
+  const int max_steps = static_cast<int>(
+      P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL);
+  int st, err = 0;
+  const bool multi = P.n_levels > 1;
+  do {
+    st = multi ? march_step<true, true>(P, r, max_steps, &dbg, &err)
+               : march_step<false, true>(P, r, max_steps, &dbg, &err);
+  } while (st == kContinue);
+  rec.steps = r.steps;
+  rec.band = r.band;
+  rec.quad = static_cast<int32_t>(
+      (r.krow - P.k) / P.n_temps - static_cast<int64_t>(r.band) * P.n_quad);
+  rec.reflections = dbg.reflections;
+  rec.term = dbg.term;
+  if (st == kFail) {
+    rec.err = err;
+    rec.err_value = dbg.err_value;
+    rec.err_axis = dbg.err_axis;
+    rec.q = r.q;
+  } else {
+    rec.q = finish_ray(P, r);
+  }
+  rec.w_abs = dbg.w_abs;
+  rec.w_walls = dbg.w_walls;
+  rec.w_res = r.tau;
+  out[s] = rec;
+  if (level_steps)
+    for (int l = 0; l < P.n_levels; ++l)
+      level_steps[s * P.n_levels + l] = dbg.level_steps[l];
+}
+
+// K2: per-cell tally in ray-id order (reference solver.cpp:142-155).
+__global__ void reduce_cells(const double* __restrict__ q_ray, int64_t n_cells,
+                             int rays, double* __restrict__ q_r,
+                             double* __restrict__ std_dev) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= n_cells) return;
+  double sum = 0.0, mean = 0.0, m2 = 0.0;
+  for (int r = 0; r < rays; ++r) {
+    const double x = q_ray[static_cast<int64_t>(r) * n_cells + c];
+    sum += x;
+    const double delta = x - mean;
+    mean += delta / (r + 1);
+    m2 += delta * (x - mean);
+  }
+  q_r[c] = sum;
+  std_dev[c] = rays > 1 ? sqrt(m2 * rays / (rays - 1.0)) : 0.0;
+}
+
+// K3: block-mean restriction (reference geometry.cpp:51-82), one thread per
+// coarse cell, fine cells summed in the reference's i, j, k loop order.
+__global__ void restrict_field(const double* __restrict__ fine, int fnx,
+                               int fny, int fnz, int ratio,
+                               double* __restrict__ coarse, int cnx, int cny,
+                               int cnz) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t n = static_cast<int64_t>(cnx) * cny * cnz;
+  if (c >= n) return;
+  const int ci = static_cast<int>(c / (static_cast<int64_t>(cny) * cnz));
+  const int cj = static_cast<int>((c / cnz) % cny);
+  const int ck = static_cast<int>(c % cnz);
+  double sum = 0.0;
+  int count = 0;
+  for (int i = ci * ratio; i < min((ci + 1) * ratio, fnx); ++i)
+    for (int j = cj * ratio; j < min((cj + 1) * ratio, fny); ++j)
+      for (int k = ck * ratio; k < min((ck + 1) * ratio, fnz); ++k) {
+        sum += fine[(static_cast<int64_t>(i) * fny + j) * fnz + k];
+        ++count;
+      }
+  coarse[c] = sum / count;
+}
+
+// Field statistics for validation and T_max (solver.cpp:27-58,
+// geometry.cpp:34-49): min, max and the count of values failing v > 0.
+__global__ void field_stats_partial(const double* __restrict__ t, int64_t n,
+                                    double* __restrict__ pmin,
+                                    double* __restrict__ pmax,
+                                    unsigned long long* __restrict__ pbad) {
+  double mn = __longlong_as_double(0x7ff0000000000000LL);
+  double mx = -mn;
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = t[i];
+    if (!(v > 0.0)) ++bad;
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  __shared__ double smn[32], smx[32];
+  __shared__ unsigned long long sbad[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+    bad += __shfl_xor_sync(kFull, bad, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    smn[w] = mn;
+    smx[w] = mx;
+    sbad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (blockDim.x >> 5); ++i) {
+      mn = fmin(mn, smn[i]);
+      mx = fmax(mx, smx[i]);
+      bad += sbad[i];
+    }
+    pmin[blockIdx.x] = mn;
+    pmax[blockIdx.x] = mx;
+    pbad[blockIdx.x] = bad;
+  }
+}
+
+__global__ void field_stats_final(const double* pmin, const double* pmax,
+                                  const unsigned long long* pbad, int nb,
+                                  double* out3) {
+  if (threadIdx.x != 0) return;
+  double mn = pmin[0], mx = pmax[0];
+  unsigned long long bad = 0;
+  for (int i = 0; i < nb; ++i) {
+    mn = fmin(mn, pmin[i]);
+    mx = fmax(mx, pmax[i]);
+    bad += pbad[i];
+  }
+  out3[0] = mn;
+  out3[1] = mx;
+  out3[2] = static_cast<double>(bad);
+}
+
+__global__ void uniform_kernel(uint64_t h_seed, int64_t n,
+                               const uint64_t* cells, const uint32_t* rays,
+                               const uint32_t* draws, double* out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  out[i] = draw_u(mix64(h_seed ^ cells[i]), rays[i], draws[i]);
+}
+
+}  // namespace
+
+// ---- host launchers -------------------------------------------------------
+
+int trace_fp64_block() { return kBlock; }
+
+int trace_fp64_blocks_per_sm(bool multi) {
+  int nb = 0;
+  if (multi)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp64<true>,
+                                                  kBlock, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp64<false>,
+                                                  kBlock, 0);
+  return nb;
+}
+
+cudaError_t launch_trace_fp64(const TraceParams& P, int grid,
+                              cudaStream_t stream) {
+  if (P.n_levels > 1)
+    trace_pool_fp64<true><<<grid, kBlock, 0, stream>>>(P);
+  else
+    trace_pool_fp64<false><<<grid, kBlock, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace_rays_fp64(const TraceParams& P, int64_t n,
+                                   const int64_t* cells,
+                                   const uint32_t* ray_ids, const double* dirs,
+                                   RayRecord* out, int64_t* level_steps,
+                                   cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int block = 64;
+  const int64_t grid = (n + block - 1) / block;
+  trace_rays_fp64<<<static_cast<unsigned>(grid), block, 0, stream>>>(
+      P, n, cells, ray_ids, dirs, out, level_steps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_cells(const double* q_ray, int64_t n_cells, int rays,
+                                double* q_r, double* std_dev,
+                                cudaStream_t stream) {
+  if (n_cells <= 0) return cudaSuccess;
+  const int block = 256;
+  reduce_cells<<<static_cast<unsigned>((n_cells + block - 1) / block), block, 0,
+                 stream>>>(q_ray, n_cells, rays, q_r, std_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_restrict(const double* fine, int fnx, int fny, int fnz,
+                            int ratio, double* coarse, int cnx, int cny,
+                            int cnz, cudaStream_t stream) {
+  const int64_t n = static_cast<int64_t>(cnx) * cny * cnz;
+  const int block = 256;
+  restrict_field<<<static_cast<unsigned>((n + block - 1) / block), block, 0,
+                   stream>>>(fine, fnx, fny, fnz, ratio, coarse, cnx, cny, cnz);
+  return cudaGetLastError();
+}
+
+// scratch: 3 * n_blocks values; out3 device [min, max, bad]
+cudaError_t launch_field_stats(const double* t, int64_t n, double* scratch,
+                               int n_blocks, double* out3,
+                               cudaStream_t stream) {
+  double* pmin = scratch;
+  double* pmax = scratch + n_blocks;
+  auto* pbad = reinterpret_cast<unsigned long long*>(scratch + 2 * n_blocks);
+  field_stats_partial<<<n_blocks, 256, 0, stream>>>(t, n, pmin, pmax, pbad);
+  field_stats_final<<<1, 32, 0, stream>>>(pmin, pmax, pbad, n_blocks, out3);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uniform(uint64_t h_seed, int64_t n, const uint64_t* cells,
+                           const uint32_t* rays, const uint32_t* draws,
+                           double* out, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int block = 256;
+  uniform_kernel<<<static_cast<unsigned>((n + block - 1) / block), block, 0,
+                   stream>>>(h_seed, n, cells, rays, draws, out);
+  return cudaGetLastError();
+}
+
+}  // namespace ermc_dev

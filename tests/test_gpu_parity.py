@@ -1,0 +1,161 @@
+"""GPU parity: the sm_100a trace kernel vs the reference CPU solver.
+
+Every test drives the product through the C-ABI (paper_1810_00188_b200.capi)
+and the checker through oracle/refshim (the unmodified reference compiled
+into oracle/_ref). Case definitions come from the reference's own
+make_case (proj/src/cases.cpp:211-295) exported through its KTAB1/TFLD1
+writers, so both sides consume identical bytes.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import refshim
+from helpers import allowed_3sigma, assert_fp64_parity, three_sigma_violations
+from paper_1810_00188_b200 import capi
+from paper_1810_00188_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+# (case, grid_n, rays, seed) — the reference's verification library at sizes
+# the CPU reference finishes in seconds.
+CASES = [
+    ("isothermal", 8, 64, 1),
+    ("grey-lin1", 10, 64, 11),
+    ("grey-parab", 12, 64, 3),
+    ("box-sin-05", 8, 32, 4),
+    ("box-sin-5", 10, 32, 2),
+    ("epsw-11", 8, 32, 6),
+    ("epsw-01", 8, 32, 8),
+    ("epsw-low", 8, 24, 5),
+    ("nb-parab", 10, 64, 7),
+    ("nb-3dimens", 8, 32, 9),
+]
+
+
+def _solve_both(grid, t, b, m, cfg):
+    g = capi.solve(grid, t, b, m, cfg)
+    r = refshim.solve(grid, t, b, m, cfg)
+    return g, r
+
+
+@pytest.mark.parametrize("name,n,rays,seed", CASES)
+def test_fp64_matches_reference(name, n, rays, seed):
+    grid, t, b, m, _ = refshim.ref_case(name, n)
+    cfg = capi.config_struct(rays_per_cell=rays, seed=seed)
+    (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(grid, t, b, m, cfg)
+    assert total == rtotal
+    assert list(steps) == list(rsteps)
+    rep = assert_fp64_parity(q, rq, sd, rsd)
+    print(name, rep)
+
+
+def test_isothermal_is_bitwise_zero():
+    # P1 (acceptance.cpp:57-74) at the reference's default 16^3, R = 500.
+    grid, t, b, m, _ = refshim.ref_case("isothermal", 0)
+    cfg = capi.config_struct(rays_per_cell=500)
+    q, sd, _, total, _ = capi.solve(grid, t, b, m, cfg)
+    assert np.all(q == 0.0) and np.all(sd == 0.0)
+    assert total > 0
+
+
+@pytest.mark.parametrize("variant", [
+    dict(specular_walls=1),
+    dict(volume_sampling=1),
+    dict(tolerance=1e-6),
+    dict(max_steps=7),
+    dict(n_levels=3, steps_per_level=4),
+    dict(n_levels=2, steps_per_level=3, coarsen_ratio=3),
+    dict(sorting=1),
+])
+def test_fp64_option_variants(variant):
+    grid, t, b, m, _ = refshim.ref_case("epsw-low", 8)
+    cfg = capi.config_struct(rays_per_cell=32, seed=21, **variant)
+    (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(grid, t, b, m, cfg)
+    assert total == rtotal, variant
+    assert list(steps) == list(rsteps), variant
+    assert_fp64_parity(q, rq, sd, rsd)
+
+
+def test_fp64_multigrid_3d_walls():
+    grid, t, b, m, _ = refshim.ref_case("nb-3dimens", 12)
+    cfg = capi.config_struct(rays_per_cell=32, seed=4, n_levels=4, steps_per_level=2)
+    (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(grid, t, b, m, cfg)
+    assert list(steps) == list(rsteps)
+    assert_fp64_parity(q, rq, sd, rsd)
+
+
+def test_fp64_channel_nongrey_matches_reference():
+    # Config 3/4 geometry and tables at a CPU-sized grid.
+    grid, t, b, m, _ = W.channel_case(16, "nongrey16")
+    cfg = capi.config_struct(rays_per_cell=32, seed=2024)
+    (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(grid, t, b, m, cfg)
+    assert total == rtotal
+    assert_fp64_parity(q, rq, sd, rsd)
+
+
+def test_fp64_channel_grey_tau_sweep():
+    for tau in (0.1, 1.0, 10.0):
+        grid, t, b, m, _ = W.channel_case(12, "grey", tau=tau)
+        cfg = capi.config_struct(rays_per_cell=16, seed=5)
+        (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(grid, t, b, m, cfg)
+        assert total == rtotal, tau
+        assert_fp64_parity(q, rq, sd, rsd)
+
+
+def test_slab_ranges_reassemble_bitwise():
+    # Multi-GPU sharding contract: x-slabs solved separately concatenate to
+    # the full solve byte for byte (GPU analogue of P8).
+    grid, t, b, m, _ = refshim.ref_case("nb-parab", 8)
+    cfg = capi.config_struct(rays_per_cell=32, seed=13)
+    q, sd, steps, total, _ = capi.solve(grid, t, b, m, cfg)
+    n = grid.nx * grid.ny * grid.nz
+    cuts = [0, 37, 64 * 3, n - 5, n]
+    qs, sds, tot = [], [], 0
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        a, s_, st, tt, _ = capi.solve(grid, t, b, m, cfg, cell_range=(lo, hi))
+        qs.append(a)
+        sds.append(s_)
+        tot += tt
+    assert np.array_equal(np.concatenate(qs), q)
+    assert np.array_equal(np.concatenate(sds), sd)
+    assert tot == total
+
+
+def test_repeat_is_deterministic():
+    grid, t, b, m, _ = refshim.ref_case("grey-parab", 8)
+    cfg = capi.config_struct(rays_per_cell=48, seed=99)
+    a = capi.solve(grid, t, b, m, cfg)
+    c = capi.solve(grid, t, b, m, cfg)
+    assert np.array_equal(a[0], c[0]) and np.array_equal(a[1], c[1]) and a[3] == c[3]
+
+
+def test_fp32_statistical_parity():
+    grid, t, b, m, _ = W.channel_case(16, "nongrey16")
+    cfg64 = capi.config_struct(rays_per_cell=64, seed=31)
+    cfg32 = capi.config_struct(rays_per_cell=64, seed=32, precision=capi.FP32)
+    q64, sd64, _, t64, _ = capi.solve(grid, t, b, m, cfg64)
+    q32, sd32, _, t32, _ = capi.solve(grid, t, b, m, cfg32)
+    n = len(q64)
+    bad = three_sigma_violations(q64, q32, sd64, sd32)
+    assert bad <= allowed_3sigma(n), (bad, n)
+    # Same seed: the fp32 kernel traces the reference's rays.
+    cfg32s = capi.config_struct(rays_per_cell=64, seed=31, precision=capi.FP32)
+    q32s, sd32s, _, t32s, _ = capi.solve(grid, t, b, m, cfg32s)
+    assert abs(t32s - t64) <= 1e-3 * t64
+    rel = np.abs(q32s - q64) / (np.abs(q64) + 1e-3 * np.max(np.abs(q64)))
+    assert np.median(rel) < 1e-3, np.median(rel)
+
+
+def test_device_rng_is_the_reference_stream():
+    rng = np.random.default_rng(5)
+    n = 20000
+    cells = rng.integers(0, 2**40, n, dtype=np.uint64)
+    rays = rng.integers(0, 2**31, n, dtype=np.uint32)
+    draws = rng.integers(0, 64, n, dtype=np.uint32)
+    for seed in (0, 17, 2**63 + 5):
+        got = capi.uniform_device(seed, cells, rays, draws)
+        want = np.array([refshim.uniform(seed, int(c), int(r), int(d))
+                         for c, r, d in zip(cells, rays, draws)])
+        assert np.array_equal(got, want)
