@@ -59,3 +59,36 @@ def three_sigma_violations(qa, qb, sda, sdb):
 
 def allowed_3sigma(n: int) -> int:
     return int(0.003 * n + 3.0 * math.sqrt(0.003 * n) + 1)
+
+
+# ---- golden fixtures -------------------------------------------------------
+from pathlib import Path as _Path  # noqa: E402
+
+GOLDEN = _Path(__file__).resolve().parent / "golden"
+CONFIG_KEYS = ["rays_per_cell", "n_levels", "tolerance", "seed", "max_steps", "sorting",
+               "steps_per_level", "coarsen_ratio", "volume_sampling", "specular_walls"]
+
+
+def golden_names():
+    return sorted(p.stem[len("solve_"):] for p in GOLDEN.glob("solve_*.npz"))
+
+
+def load_model(z):
+    from paper_1810_00188_b200 import capi
+    return capi.ModelArrays(z["m_nu_lo"], z["m_nu_hi"], z["m_nu_center"], z["m_g"], z["m_w"],
+                            z["m_temps"], z["m_k"], z["m_ib"])
+
+
+def load_golden_solve(name):
+    """(grid, T, boundary, model, config, expected dict) of a golden solve."""
+    from paper_1810_00188_b200 import capi
+    z = np.load(GOLDEN / f"solve_{name}.npz")
+    grid = capi.make_grid(z["grid_n"], z["grid_d"], z["grid_origin"])
+    b = capi.make_boundary(z["b_kind"], list(zip(z["b_lo_t"], z["b_lo_e"])),
+                           list(zip(z["b_hi_t"], z["b_hi_e"])))
+    cfg_vals = dict(zip(CONFIG_KEYS, z["config"].tolist()))
+    ints = {k: int(v) for k, v in cfg_vals.items() if k != "tolerance"}
+    cfg = capi.config_struct(tolerance=cfg_vals["tolerance"], **ints)
+    expected = dict(q_r=z["q_r"], std_dev=z["std_dev"], steps=z["steps_per_level"],
+                    total=int(z["total_steps"][0]))
+    return grid, z["temperature"], b, load_model(z), cfg, expected
