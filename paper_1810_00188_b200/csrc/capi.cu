@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -26,12 +27,14 @@
 #include "trace_common.cuh"
 
 namespace ermc_dev {
-int trace_fp64_block();
-int trace_fp64_blocks_per_sm(bool multi);
-cudaError_t launch_trace_fp64(const TraceParams& P, int grid, cudaStream_t s);
-int trace_fp32_block();
-int trace_fp32_blocks_per_sm(bool multi);
-cudaError_t launch_trace_fp32(const TraceParams& P, int grid, cudaStream_t s);
+int trace_fp64_blocks_per_sm(const TraceParams& P, int min_blocks);
+cudaError_t launch_trace_fp64(const TraceParams& P, int grid, int min_blocks,
+                              cudaStream_t s);
+int trace_fp32_blocks_per_sm(const TraceParams& P, int min_blocks);
+cudaError_t launch_trace_fp32(const TraceParams& P, int grid, int min_blocks,
+                              cudaStream_t s);
+cudaError_t launch_build_iv64(const double* k, const double* ib, int nb,
+                              int nq, int nt, double4* iv, cudaStream_t s);
 cudaError_t launch_trace_rays_fp64(const TraceParams& P, int64_t n,
                                    const int64_t* cells, const uint32_t* rays,
                                    const double* dirs, RayRecord* out,
@@ -170,6 +173,30 @@ struct Timing {
   cudaEvent_t a = nullptr, b = nullptr;
 };
 
+// Scheduling knobs (defaults tuned on B200; ERMC_* environment variables
+// override them for experiments — they never change results).
+struct Tune {
+  int inner_steps = 4;
+  int refill = 4;
+  int fp64_min_blocks = 4;
+  int fp32_min_blocks = 6;
+};
+int env_int(const char* name, int fallback) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : fallback;
+}
+const Tune& tune() {
+  static const Tune t = [] {
+    Tune x;
+    x.inner_steps = std::max(1, env_int("ERMC_INNER_STEPS", x.inner_steps));
+    x.refill = std::max(1, std::min(32, env_int("ERMC_REFILL", x.refill)));
+    x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
+    x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
+    return x;
+  }();
+  return t;
+}
+
 }  // namespace
 
 struct ermc_session {
@@ -187,6 +214,7 @@ struct ermc_session {
   DevBuf<double> d_temps, d_k, d_ib, d_wall_ib, d_band_cdf, d_quad_cdf, d_kmax,
       d_ibmax;
   DevBuf<float> d_wall_ibn32;
+  DevBuf<double4> d_tint, d_iv64;
   DevBuf<double> d_field;
   std::vector<std::unique_ptr<DevBuf<double>>> d_levels;  // levels >= 1
   std::vector<ermc_grid_t> level_grids;
@@ -268,6 +296,22 @@ ermc_session* create_session(const ermc_grid_t* grid,
   s->d_temps.upload(s->temps.data(), s->temps.size(), st);
   s->d_k.upload(s->k.data(), s->k.size(), st);
   s->d_ib.upload(s->ib.data(), s->ib.size(), st);
+  {
+    // Packed fp64 tables (copies of reference values + exact reciprocals).
+    const ermc_host::TableView& v = s->view;
+    if (v.nt >= 2) {
+      std::vector<double4> tint(v.nt - 1);
+      for (int l = 0; l + 1 < v.nt; ++l) {
+        const double w = v.temps[l + 1] - v.temps[l];
+        tint[l] = make_double4(v.temps[l], w, 1.0 / w, 0.0);
+      }
+      s->d_tint.upload(tint.data(), tint.size(), st);
+      s->d_iv64.ensure(static_cast<size_t>(v.nb) * v.nq * (v.nt - 1));
+      cuda_check(ermc_dev::launch_build_iv64(s->d_k.p, s->d_ib.p, v.nb, v.nq, v.nt,
+                                             s->d_iv64.p, st),
+                 "build_iv64");
+    }
+  }
   s->d_field.ensure(static_cast<size_t>(s->n_cells));
   s->d_stats_scratch.ensure(3 * kStatsBlocks);
   s->d_stats.ensure(3);
@@ -470,7 +514,14 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.volume_sampling = c.volume_sampling;
   P.h_seed = mix64_host(c.seed + 0x9e3779b97f4a7c15ULL);
   P.rays = c.rays_per_cell;
-  P.refill_threshold = 4;
+  P.refill_threshold = tune().refill;
+  P.inner_steps = tune().inner_steps;
+  P.tol32 = static_cast<float>(c.tolerance);
+  P.tint = s->d_tint.p;
+  P.iv64 = s->d_iv64.p;
+  P.inv_dt = 1.0 / v.dt;
+  P.t_first = v.temps[0];
+  P.t_last = v.temps[v.nt - 1];
   P.steps_per_level = s->d_steps.p;
 }
 
@@ -560,9 +611,9 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
              "memset");
   cuda_check(cudaMemsetAsync(s->d_steps.p, 0, ermc_dev::kMaxLevels * sizeof(unsigned long long), st),
              "memset");
-  const bool multi = s->config.n_levels > 1;
-  const int bps = fp32 ? ermc_dev::trace_fp32_blocks_per_sm(multi)
-                       : ermc_dev::trace_fp64_blocks_per_sm(multi);
+  const int min_blocks = fp32 ? tune().fp32_min_blocks : tune().fp64_min_blocks;
+  const int bps = fp32 ? ermc_dev::trace_fp32_blocks_per_sm(P, min_blocks)
+                       : ermc_dev::trace_fp64_blocks_per_sm(P, min_blocks);
   const int grid = std::max(1, bps) * s->n_sm;
 
   std::vector<Timing> tt(n_chunks), tr(n_chunks);
@@ -581,8 +632,8 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
     cudaEventCreate(&tr[ch].a);
     cudaEventCreate(&tr[ch].b);
     cudaEventRecord(tt[ch].a, st);
-    cuda_check(fp32 ? ermc_dev::launch_trace_fp32(P, grid, st)
-                    : ermc_dev::launch_trace_fp64(P, grid, st),
+    cuda_check(fp32 ? ermc_dev::launch_trace_fp32(P, grid, min_blocks, st)
+                    : ermc_dev::launch_trace_fp64(P, grid, min_blocks, st),
                "trace");
     cudaEventRecord(tt[ch].b, st);
     cudaEventRecord(tr[ch].a, st);

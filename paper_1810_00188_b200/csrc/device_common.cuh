@@ -35,6 +35,16 @@ __device__ __forceinline__ double draw_u(uint64_t h_cell, uint32_t ray,
   return static_cast<double>(h >> 11) * 0x1.0p-53;
 }
 
+// One 32-byte read-only load (LDG.E.ENL2.256 on sm_100a): a whole interval
+// record in one sector.
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+  double4 r;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+      : "l"(p));
+  return r;
+}
+
 // std::upper_bound over a short ascending array (sampling.cpp:44-51).
 __device__ __forceinline__ int upper_bound_d(const double* a, int n, double x) {
   int first = 0, count = n;
@@ -168,7 +178,11 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         pool_next >= pool_end)
       break;
     if (active) {
-      const int st = tr.step(P, max_steps);
+      // Several march steps per pool check: amortises the ballots; a lane
+      // whose ray ends early idles for < inner_steps iterations.
+      int st = kContinue;
+      for (int s = 0; s < P.inner_steps && st == kContinue; ++s)
+        st = tr.step(P, max_steps);
       if (st != kContinue) {
         active = false;
         if (st == kDone) {

@@ -54,12 +54,19 @@ struct TraceParams {
   const double* quad_cdf;    // [n_bands][n_quad]
   const double* k_max;       // [n_bands][n_quad]  k(n,g,T_max)
   const double* ib_max;      // [n_bands]          Ib(n,T_max)
+  // Packed fp64 tables of the fast single-level kernel (values are copies, so
+  // interpolation stays bitwise the reference's):
+  const double4* tint;       // [n_temps-1] {t_lo, t_hi - t_lo, 1/(t_hi - t_lo), 0}
+  const double4* iv64;       // [n_bands*n_quad][n_temps-1] {k_lo, k_hi, ib_lo, ib_hi}
+  double inv_dt;             // 1/dt for the table-index estimate
+  double t_first, t_last;    // table range
 
   // ---- fp32 fast-path tables (trace_fp32.cu) ----
   const float4* iv32;        // [n_bands*n_quad][n_temps-1] {k_lo, k_hi-k_lo, ib_lo, ib_hi-ib_lo}
   const float* wall_ibn32;   // [6][n_bands] wall Ib / Ib(n, T_last)
   float inv_dt32;            // 1/dt for the fp32 lookup (uniform grids only)
   float t0_32;
+  float tol32;               // tolerance as float
 
   // ---- march options (TraceOptions, tracer.hpp:26-30) ----
   double qe;                 // 4 kappa_p(T_max) sigma T_max^4 / R (solver.cpp:92-93)
@@ -72,6 +79,7 @@ struct TraceParams {
 
   // ---- work decomposition ----
   int32_t refill_threshold;  // idle lanes before a warp regenerates rays
+  int32_t inner_steps;       // march steps between two pool checks
   int64_t cell_base;         // first global linear cell of this chunk
   int64_t n_cells;           // cells in this chunk
   uint64_t n_work;           // n_cells * rays (ray work items)

@@ -51,15 +51,14 @@ struct Fp32Tracer {
   double cq;     // QE * k1/k_max * Ib(T_last)/Ib_max  (per ray)
   const float4* row;
   int idx[3], stp[3];
-  int dlin[3];   // signed linear stride of one step on each axis
-  int lin;
+  int lin;       // linear index of the current cell
+  float t_cur;   // its temperature (prefetched one step ahead)
   int band, lvl, sal_, steps_;
   uint32_t next_draw, ray_id;
   uint64_t h_cell;
   int err;
 
   __device__ __forceinline__ void setup(const LevelDesc& L) {
-    const int stride[3] = {L.n[1] * L.n[2], L.n[2], 1};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const float da = dir[a];
@@ -67,12 +66,10 @@ struct Fp32Tracer {
         tn[a] = __int_as_float(0x7f800000);
         td[a] = __int_as_float(0x7f800000);
         stp[a] = 0;
-        dlin[a] = 0;
         continue;
       }
       const float inv = 1.0f / da;
       stp[a] = da > 0.0f ? 1 : -1;
-      dlin[a] = da > 0.0f ? stride[a] : -stride[a];
       const float face = static_cast<float>(
           L.origin[a] + (idx[a] + (da > 0.0f ? 1 : 0)) * L.d[a]);
       tn[a] = (face - p0[a]) * inv;
@@ -150,12 +147,13 @@ struct Fp32Tracer {
     sal_ = 0;
     steps_ = 0;
     setup(L);
+    t_cur = t_cell;
     return kErrNone;
   }
 
   template <bool kMulti>
   __device__ __forceinline__ int step_t(const TraceParams& P, int max_steps) {
-    if (tau <= static_cast<float>(P.tol)) return kDone;
+    if (tau <= P.tol32) return kDone;
     if (steps_ >= max_steps) return kDone;
     if (kMulti) {
       const int cap = P.lv[lvl].cap;
@@ -174,9 +172,16 @@ struct Fp32Tracer {
         }
         sal_ = 0;
         setup(C);
+        t_cur = __ldg(C.field32 + lin);
       }
     }
     const LevelDesc& L = P.lv[kMulti ? lvl : 0];
+    // table record of the current cell (its T arrived during the last step)
+    const float u = fmaf(t_cur, P.inv_dt32, -P.t0_32 * P.inv_dt32);
+    const int lo = min(max(static_cast<int>(u), 0), P.n_temps - 2);
+    const float f = u - static_cast<float>(lo);
+    const float4 v = __ldg(row + lo);
+
     int axis = 0;
     float tmin = tn[0];
     if (tn[1] < tmin) {
@@ -190,11 +195,23 @@ struct Fp32Tracer {
     const float ds = fmaxf(tmin - s, 0.0f);
     s = fmaxf(tmin, s);
 
-    const float t_cell = __ldg(L.field32 + lin);
-    const float u = fmaf(t_cell, P.inv_dt32, -P.t0_32 * P.inv_dt32);
-    const int lo = min(max(static_cast<int>(u), 0), P.n_temps - 2);
-    const float f = u - static_cast<float>(lo);
-    const float4 v = __ldg(row + lo);
+    // next cell; its T is fetched now, ahead of this step's math
+    int ia = 0, na = 0, sa = 0, stride = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) {
+        sa = stp[a];
+        ia = idx[a] + sa;
+        na = L.n[a];
+        stride = a == 0 ? L.n[1] * L.n[2] : (a == 1 ? L.n[2] : 1);
+        tn[a] += td[a];
+      }
+    const bool inside = ia >= 0 && ia < na;
+    int nlin = lin + (sa > 0 ? stride : -stride);
+    if (!inside) nlin += (ia < 0 ? 1 : -1) * stride * na;  // periodic image
+    float t_next = t_cur;
+    if (inside || P.periodic[axis]) t_next = __ldg(L.field32 + nlin);
+
     const float kappa = fmaf(f, v.y, v.x);
     const float ib2n = fmaf(f, v.w, v.z);
     const float alpha = absorb32(kappa * ds);
@@ -202,22 +219,17 @@ struct Fp32Tracer {
     const float ta = tau * alpha;
     acc = fmaf(ta, ib2n - ib1n, acc);
     tau -= ta;
-
-    int ia = 0, na = 0, sa = 0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-      if (a == axis) {
-        tn[a] += td[a];
-        idx[a] += stp[a];
-        lin += dlin[a];
-        ia = idx[a];
-        na = L.n[a];
-        sa = stp[a];
-      }
     ++steps_;
     if (kMulti) ++sal_;
-    if (ia >= 0 && ia < na) return kContinue;
 
+    if (inside) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) idx[a] = ia;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
     if (P.periodic[axis]) {
       rebase();
       const float ext = static_cast<float>(L.extent[axis]);
@@ -232,11 +244,12 @@ struct Fp32Tracer {
             p0[a] -= ext;
           }
         }
-      lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
+      lin = nlin;
+      t_cur = t_next;
       return kContinue;
     }
 
-    // wall exchange (tracer.cpp:155-165)
+    // wall exchange (tracer.cpp:155-165); the ray stays in its cell
     const bool at_hi = sa > 0;
     const int face = 2 * axis + (at_hi ? 1 : 0);
     const float ew = static_cast<float>(P.wall_eps[face]);
@@ -244,7 +257,7 @@ struct Fp32Tracer {
     const float tw = tau * ew;
     acc = fmaf(tw, ibw - ib1n, acc);
     tau -= tw;
-    if (tau <= static_cast<float>(P.tol)) return kDone;
+    if (tau <= P.tol32) return kDone;
     // reflection (tracer.cpp:167-182)
     rebase();
     const float face_pos = static_cast<float>(
@@ -273,10 +286,7 @@ struct Fp32Tracer {
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      if (a == axis) {
-        idx[a] -= stp[a];
-        p0[a] = face_pos;
-      }
+      if (a == axis) p0[a] = face_pos;
       dir[a] = nd[a];
     }
     setup(L);
@@ -306,8 +316,8 @@ struct Fp32Multi : Fp32Tracer {
   }
 };
 
-template <bool kMulti>
-__global__ void __launch_bounds__(kBlock32, 6)
+template <bool kMulti, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32(const __grid_constant__ TraceParams P) {
   if (kMulti)
     pool_kernel_body<Fp32Multi, true>(P);
@@ -347,23 +357,24 @@ __global__ void to_fp32(const double* __restrict__ src, float* __restrict__ dst,
 
 int trace_fp32_block() { return kBlock32; }
 
-int trace_fp32_blocks_per_sm(bool multi) {
+namespace {
+using TraceFn32 = void (*)(TraceParams);
+TraceFn32 fp32_kernel(bool multi, int min_blocks) {
+  if (multi) return min_blocks >= 8 ? trace_pool_fp32<true, 8> : trace_pool_fp32<true, 6>;
+  return min_blocks >= 8 ? trace_pool_fp32<false, 8> : trace_pool_fp32<false, 6>;
+}
+}  // namespace
+
+int trace_fp32_blocks_per_sm(const TraceParams& P, int min_blocks) {
   int nb = 0;
-  if (multi)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp32<true>,
-                                                  kBlock32, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp32<false>,
-                                                  kBlock32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &nb, fp32_kernel(P.n_levels > 1, min_blocks), kBlock32, 0);
   return nb;
 }
 
-cudaError_t launch_trace_fp32(const TraceParams& P, int grid,
+cudaError_t launch_trace_fp32(const TraceParams& P, int grid, int min_blocks,
                               cudaStream_t stream) {
-  if (P.n_levels > 1)
-    trace_pool_fp32<true><<<grid, kBlock32, 0, stream>>>(P);
-  else
-    trace_pool_fp32<false><<<grid, kBlock32, 0, stream>>>(P);
+  fp32_kernel(P.n_levels > 1, min_blocks)<<<grid, kBlock32, 0, stream>>>(P);
   return cudaGetLastError();
 }
 

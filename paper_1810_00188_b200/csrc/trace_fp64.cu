@@ -376,6 +376,266 @@ __device__ __forceinline__ double finish_ray(const TraceParams& P,
   return r.q + P.qe * r.tau * ((r.last_ib2 - r.ib1) / r.ib1) * r.pref;
 }
 
+// ---------------------------------------------------------------------------
+// Fast single-level tracer. Same operations, same order, same rounding as
+// march_step (hence the reference), restructured for the gather latency:
+//   * T of the next cell is loaded one step ahead, while the current step's
+//     absorption math runs (the DDA does not depend on absorption);
+//   * one 32-byte interval record {k_lo, k_hi, ib_lo, ib_hi} per step instead
+//     of four scattered loads, and {t_lo, w, 1/w} per temperature interval;
+//   * divisions by a per-ray or per-interval constant use its correctly
+//     rounded reciprocal plus one FMA correction (Markstein), which returns
+//     the correctly rounded quotient, i.e. bitwise the IEEE division;
+//   * the table index estimate (T - t0) * (1/dt) falls back to the true
+//     division near an integer, so trunc() sees the reference's quotient.
+
+// Correctly rounded a / b from r = RN(1/b) (Markstein / Cornea et al.).
+__device__ __forceinline__ double div_rcp(double a, double b, double r) {
+  const double q0 = a * r;
+  const double e = fma(-q0, b, a);
+  return fma(e, r, q0);
+}
+
+// SpectralModel::lookup on the packed tables (uniform or not).
+__device__ __forceinline__ bool fast_lookup(const TraceParams& P, double T,
+                                            int& lo, double& frac) {
+  if (!(T >= P.t_first && T <= P.t_last)) return false;
+  const int nt = P.n_temps;
+  int l;
+  if (P.uniform_temps) {
+    const double x = (T - P.t0) * P.inv_dt;
+    const double xf = x - floor(x);
+    if (xf < 1e-9 || xf > 1.0 - 1e-9)
+      l = static_cast<int>((T - P.t0) / P.dt);  // the reference's quotient
+    else
+      l = static_cast<int>(x);
+    l = min(max(l, 0), nt - 2);
+    double4 ti = ldg4(P.tint + l);
+    double f = div_rcp(T - ti.x, ti.y, ti.z);
+    if (f < 0.0 && l > 0) {
+      --l;
+      ti = ldg4(P.tint + l);
+      f = div_rcp(T - ti.x, ti.y, ti.z);
+    } else if (f > 1.0 && l < nt - 2) {
+      ++l;
+      ti = ldg4(P.tint + l);
+      f = div_rcp(T - ti.x, ti.y, ti.z);
+    }
+    lo = l;
+    frac = f;
+    return true;
+  }
+  const int hi = upper_bound_d(P.temps, nt, T);
+  if (hi == 0) {
+    lo = 0;
+    frac = 0.0;
+  } else if (hi == nt) {
+    lo = nt - 2;
+    frac = 1.0;
+  } else {
+    lo = hi - 1;
+    const double4 ti = ldg4(P.tint + lo);
+    frac = div_rcp(T - ti.x, ti.y, ti.z);
+  }
+  return true;
+}
+
+struct Fp64Fast {
+  double pos[3], dir[3], tn[3], td[3];
+  double tau, q, last_ib2, ib1, rib1, pref, t_cur;
+  const double4* row;
+  int64_t lin;
+  int idx[3];
+  int band, steps_;
+  uint32_t next_draw, ray_id;
+  uint64_t h_cell;
+  int err;
+
+  __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
+                                      uint32_t ray) {
+    Ray r;
+    const int e = init_ray(P, cell, ray, r, nullptr);
+    if (e != kErrNone) return e;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      pos[a] = r.pos[a];
+      dir[a] = r.dir[a];
+      tn[a] = r.tn[a];
+      td[a] = r.td[a];
+      idx[a] = r.idx[a];
+    }
+    tau = 1.0;
+    q = 0.0;
+    ib1 = r.ib1;
+    last_ib2 = r.ib1;
+    rib1 = 1.0 / r.ib1;
+    pref = r.pref;
+    band = r.band;
+    const int64_t ng = (r.krow - P.k) / P.n_temps;
+    row = P.iv64 + ng * (P.n_temps - 1);
+    steps_ = 0;
+    next_draw = r.next_draw;
+    ray_id = ray;
+    h_cell = r.h_cell;
+    lin = cell;
+    t_cur = __ldg(P.lv[0].field + cell);
+    return kErrNone;
+  }
+
+  __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
+    if (tau <= P.tol) return kDone;
+    if (steps_ >= max_steps) return kDone;
+    const LevelDesc& L = P.lv[0];
+    int lo;
+    double frac;
+    if (!fast_lookup(P, t_cur, lo, frac)) {
+      err = kErrTableRange;
+      return kFail;
+    }
+    const double4 v = ldg4(row + lo);  // {k_lo, k_hi, ib_lo, ib_hi}
+
+    int axis = 0;
+    double ds = tn[0];
+    if (tn[1] < ds) {
+      ds = tn[1];
+      axis = 1;
+    }
+    if (tn[2] < ds) {
+      ds = tn[2];
+      axis = 2;
+    }
+    if (ds < 0.0) ds = 0.0;
+
+    // Next cell, and its temperature prefetched ahead of this step's math.
+    int ia = 0, na = 0, sa = 0;
+    int64_t stride = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) {
+        sa = dir[a] > 0.0 ? 1 : -1;
+        ia = idx[a] + sa;
+        na = L.n[a];
+        stride = a == 0 ? static_cast<int64_t>(L.n[1]) * L.n[2]
+                        : (a == 1 ? static_cast<int64_t>(L.n[2]) : 1);
+      }
+    const bool inside = ia >= 0 && ia < na;
+    int64_t nlin = lin + (sa > 0 ? stride : -stride);
+    if (!inside) nlin += (ia < 0 ? 1 : -1) * stride * na;  // periodic image
+    double t_next = t_cur;
+    if (inside || P.periodic[axis]) t_next = __ldg(L.field + nlin);
+
+    const double kappa = frac == 0.0 ? v.x : v.x + frac * (v.y - v.x);
+    const double ib2 = frac == 0.0 ? v.z : v.z + frac * (v.w - v.z);
+    const double alpha = -expm1(-kappa * ds);
+    last_ib2 = ib2;
+    q += P.qe * tau * alpha * div_rcp(ib2 - ib1, ib1, rib1) * pref;
+    tau *= 1.0 - alpha;
+
+    const double advance = ds + L.eps;
+    pos[0] += advance * dir[0];
+    pos[1] += advance * dir[1];
+    pos[2] += advance * dir[2];
+    tn[0] -= advance;
+    tn[1] -= advance;
+    tn[2] -= advance;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) tn[a] += td[a];
+    ++steps_;
+
+    if (inside) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) idx[a] = ia;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    if (P.periodic[axis]) {
+      const double ext = L.extent[axis];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) {
+          if (ia < 0) {
+            idx[a] = na - 1;
+            pos[a] += ext;
+          } else {
+            idx[a] = 0;
+            pos[a] -= ext;
+          }
+        }
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    // Wall exchange, absorption or reflection (tracer.cpp:155-184); the ray
+    // stays in its boundary cell, so lin and t_cur are unchanged.
+    const bool at_hi = sa > 0;
+    const int face = 2 * axis + (at_hi ? 1 : 0);
+    const double ew = P.wall_eps[face];
+    const double ib_w = __ldg(P.wall_ib + face * P.n_bands + band);
+    q += P.qe * tau * ew * div_rcp(ib_w - ib1, ib1, rib1) * pref;
+    tau *= 1.0 - ew;
+    if (tau <= P.tol) return kDone;
+    const double face_pos = L.origin[axis] + (at_hi ? L.extent[axis] : 0.0);
+    const int inward = at_hi ? -1 : 1;
+    double nd[3] = {dir[0], dir[1], dir[2]};
+    if (P.specular) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) nd[a] = -nd[a];
+    } else {
+      const double r1 = draw_u(h_cell, ray_id, next_draw++);
+      const double r2 = draw_u(h_cell, ray_id, next_draw++);
+      const double sin_t = sqrt(r1);
+      const double cos_t = sqrt(1.0 - r1);
+      const double phi = 2.0 * kPiD * r2;
+      double sp, cp;
+      sincos(phi, &sp, &cp);
+      const int t1 = axis == 2 ? 0 : axis + 1;
+      const int t2 = axis == 0 ? 2 : axis - 1;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a == axis) nd[a] = inward * cos_t;
+        if (a == t1) nd[a] = sin_t * cp;
+        if (a == t2) nd[a] = sin_t * sp;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a == axis) pos[a] = face_pos;
+      dir[a] = nd[a];
+    }
+    pos[0] += L.eps * dir[0];
+    pos[1] += L.eps * dir[1];
+    pos[2] += L.eps * dir[2];
+    // Dda::setup (tracer.cpp:17-38)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double da = dir[a];
+      if (da == 0.0) {
+        tn[a] = __longlong_as_double(0x7ff0000000000000LL);
+        td[a] = __longlong_as_double(0x7ff0000000000000LL);
+        continue;
+      }
+      const int face_idx = idx[a] + (da > 0.0 ? 1 : 0);
+      const double fpos = L.origin[a] + face_idx * L.d[a];
+      tn[a] = (fpos - pos[a]) / da;
+      td[a] = L.d[a] / fabs(da);
+    }
+    return kContinue;
+  }
+
+  // Residual dump (tracer.cpp:186-188).
+  __device__ __forceinline__ double finish(const TraceParams& P) const {
+    return q + P.qe * tau * div_rcp(last_ib2 - ib1, ib1, rib1) * pref;
+  }
+  __device__ __forceinline__ bool finite_state() const { return isfinite(tau); }
+  __device__ __forceinline__ int level() const { return 0; }
+  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int steps() const { return steps_; }
+};
+
 struct Fp64Tracer {
   Ray r;
   int err;
@@ -411,13 +671,16 @@ struct Fp64Multi : Fp64Tracer {
 constexpr int kBlock = 128;
 
 // K1: persistent ray-pool trace over the chunk's (cell, ray) work items.
-template <bool kMulti>
-__global__ void __launch_bounds__(kBlock, 4)
+// kMulti = false: the fast single-level tracer; true: the reference-order
+// tracer with multigrid demotion (also used for single-node tables).
+// kMinBlocks trades registers for occupancy (tuned on B200).
+template <bool kMulti, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64(const __grid_constant__ TraceParams P) {
   if (kMulti)
     pool_kernel_body<Fp64Multi, true>(P);
   else
-    pool_kernel_body<Fp64Single, false>(P);
+    pool_kernel_body<Fp64Fast, false>(P);
 }
 
 // Debug/test kernel: one thread traces one explicit ray with full
@@ -586,6 +849,21 @@ __global__ void field_stats_final(const double* pmin, const double* pmax,
   out3[2] = static_cast<double>(bad);
 }
 
+// Packed fp64 tables for the fast tracer (copies of reference values).
+__global__ void build_iv64(const double* __restrict__ k,
+                           const double* __restrict__ ib, int nb, int nq,
+                           int nt, double4* __restrict__ iv) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t n_iv = static_cast<int64_t>(nb) * nq * (nt - 1);
+  if (i >= n_iv) return;
+  const int t = static_cast<int>(i % (nt - 1));
+  const int64_t ng = i / (nt - 1);
+  const int n = static_cast<int>(ng / nq);
+  const double* krow = k + ng * nt;
+  const double* ibrow = ib + static_cast<int64_t>(n) * nt;
+  iv[i] = make_double4(krow[t], krow[t + 1], ibrow[t], ibrow[t + 1]);
+}
+
 __global__ void uniform_kernel(uint64_t h_seed, int64_t n,
                                const uint64_t* cells, const uint32_t* rays,
                                const uint32_t* draws, double* out) {
@@ -600,23 +878,29 @@ __global__ void uniform_kernel(uint64_t h_seed, int64_t n,
 
 int trace_fp64_block() { return kBlock; }
 
-int trace_fp64_blocks_per_sm(bool multi) {
+namespace {
+// Kernel variant by (path, min blocks per SM); 4 or 5 blocks of 128 threads.
+using TraceFn = void (*)(TraceParams);
+TraceFn fp64_kernel(bool multi, int min_blocks) {
+  if (multi) return min_blocks >= 5 ? trace_pool_fp64<true, 5> : trace_pool_fp64<true, 4>;
+  return min_blocks >= 5 ? trace_pool_fp64<false, 5> : trace_pool_fp64<false, 4>;
+}
+}  // namespace
+
+bool fp64_fast_path(const TraceParams& P) {
+  return P.n_levels == 1 && P.n_temps >= 2;
+}
+
+int trace_fp64_blocks_per_sm(const TraceParams& P, int min_blocks) {
   int nb = 0;
-  if (multi)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp64<true>,
-                                                  kBlock, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, trace_pool_fp64<false>,
-                                                  kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &nb, fp64_kernel(!fp64_fast_path(P), min_blocks), kBlock, 0);
   return nb;
 }
 
-cudaError_t launch_trace_fp64(const TraceParams& P, int grid,
+cudaError_t launch_trace_fp64(const TraceParams& P, int grid, int min_blocks,
                               cudaStream_t stream) {
-  if (P.n_levels > 1)
-    trace_pool_fp64<true><<<grid, kBlock, 0, stream>>>(P);
-  else
-    trace_pool_fp64<false><<<grid, kBlock, 0, stream>>>(P);
+  fp64_kernel(!fp64_fast_path(P), min_blocks)<<<grid, kBlock, 0, stream>>>(P);
   return cudaGetLastError();
 }
 
@@ -662,6 +946,15 @@ cudaError_t launch_field_stats(const double* t, int64_t n, double* scratch,
   auto* pbad = reinterpret_cast<unsigned long long*>(scratch + 2 * n_blocks);
   field_stats_partial<<<n_blocks, 256, 0, stream>>>(t, n, pmin, pmax, pbad);
   field_stats_final<<<1, 32, 0, stream>>>(pmin, pmax, pbad, n_blocks, out3);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_iv64(const double* k, const double* ib, int nb, int nq,
+                              int nt, double4* iv, cudaStream_t stream) {
+  const int64_t n = static_cast<int64_t>(nb) * nq * (nt - 1);
+  if (n <= 0) return cudaSuccess;
+  build_iv64<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+      k, ib, nb, nq, nt, iv);
   return cudaGetLastError();
 }
 
