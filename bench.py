@@ -129,39 +129,56 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU arm
+class CpuReference:
+    """The reference solver (oracle/_ref: unmodified sources) on a stratified
+    sample of the workload's cells, through the cell-subset replay of
+    solver.cpp:118-156 (bitwise the reference's solve() for those cells).
+    The timing covers the march loop, not the O(N) per-call setup copies."""
+
+    def __init__(self, grid, t, b, m, cfg, threads):
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import refshim  # noqa: PLC0415
+
+        self.n = grid.nx * grid.ny * grid.nz
+        self.threads = threads
+        if refshim.available():
+            self.run = lambda cells: refshim.solve_cells(grid, t, b, m, cfg, cells,
+                                                         threads=threads)
+            self.kind = "reference"
+        else:  # the C restatement (port) if the reference could not be built
+            import oracle  # noqa: PLC0415
+
+            def run(cells):
+                t0 = time.perf_counter()
+                lo, hi = int(cells[0]), int(cells[-1]) + 1
+                q, sd, st, tot = oracle.solve(grid, t, b, m, cfg, cell_range=(lo, hi),
+                                              threads=threads)
+                return q, sd, st, time.perf_counter() - t0
+            self.run = run
+            self.kind = "port"
+        self.cells = None
+
+    def size(self, seconds):
+        want = max(self.threads * 4, 32)
+        while True:
+            cells = np.unique(np.linspace(0, self.n - 1, min(self.n, want)).astype(np.int64))
+            _, _, st, wall = self.run(cells)
+            if wall >= 0.5 * seconds or len(cells) >= self.n:
+                break
+            want = int(want * min(8.0, max(1.5, 0.9 * seconds / max(wall, 1e-3))))
+        self.cells = cells
+
+    def step(self):
+        _, _, st, wall = self.run(self.cells)
+        steps = int(np.sum(st))
+        return steps / wall, steps, wall, len(self.cells)
+
+
 def cpu_reference_sample(grid, t, b, m, cfg, seconds, threads):
-    """Times the reference solver (oracle/_ref: unmodified sources) on a
-    stratified sample of cells sized for ~`seconds` of work with `threads`
-    host threads. Returns (steps/s, steps, wall, n_cells, kind)."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import refshim  # noqa: PLC0415
-
-    n = grid.nx * grid.ny * grid.nz
-    if refshim.available():
-        run = lambda cells: refshim.solve_cells(grid, t, b, m, cfg, cells, threads=threads)  # noqa: E731
-        kind = "reference"
-    else:  # C restatement (port) when the reference could not be built
-        import oracle  # noqa: PLC0415
-
-        def run(cells):
-            q, sd, st, tot = oracle.solve(grid, t, b, m, cfg, cell_range=(int(cells[0]),
-                                                                           int(cells[-1]) + 1),
-                                          threads=threads)
-            return q, sd, st, 0.0
-        kind = "port"
-    probe = max(threads * 2, 16)
-    cells = np.linspace(0, n - 1, probe).astype(np.int64)
-    t0 = time.perf_counter()
-    _, _, st, _ = run(cells)
-    dt = time.perf_counter() - t0
-    rate_cells = probe / max(dt, 1e-3)
-    want = int(min(n, max(probe, rate_cells * seconds)))
-    cells = np.unique(np.linspace(0, n - 1, want).astype(np.int64))
-    t0 = time.perf_counter()
-    _, _, st, _ = run(cells)
-    wall = time.perf_counter() - t0
-    steps = int(np.sum(st))
-    return steps / wall, steps, wall, len(cells), kind
+    ref = CpuReference(grid, t, b, m, cfg, threads)
+    ref.size(seconds)
+    v, steps, wall, n = ref.step()
+    return v, steps, wall, n, ref.kind
 
 
 def run_reference(a, world, rank):
@@ -172,14 +189,15 @@ def run_reference(a, world, rank):
     grid, t, b, m, _ = W.channel_case(a.grid, a.model)
     cfg = capi.config_struct(rays_per_cell=a.rays, seed=a.seed, workers=os.cpu_count() or 1)
     threads = os.cpu_count() or 1
-    per_step = max(5.0, min(a.cpu_seconds, 20.0))
+    ref = CpuReference(grid, t, b, m, cfg, threads)
+    ref.size(max(5.0, min(a.cpu_seconds, 20.0)))
     vals = []
     last = None
     for i in range(a.warmup + a.steps):
-        r = cpu_reference_sample(grid, t, b, m, cfg, per_step if i >= a.warmup else 3.0, threads)
+        r = ref.step()
         if i >= a.warmup:
             vals.append(r[0])
-            last = r
+            last = r + (ref.kind,)
     value = sum(vals) / len(vals)
     n_cells = a.grid ** 3
     sample = (f"{last[3]} stratified cells of {n_cells} x R={a.rays} "
@@ -289,12 +307,16 @@ def run_b200(a, world, rank, local):
     peak, peak_kind = peaks()
     bps = BYTES_PER_STEP[a.precision]
     achieved = local_steps * bps / (trace_ms * 1e-3) / 1e9  # GB/s of the trace kernel
+    # DRAM traffic per launch: bytes/step of the committed `ncu --set full`
+    # capture (profiles/ncu_trace_summary.json, same kernel, 256^3 channel)
+    # times the steps of one launch here.
     traffic = None
     prof = ROOT / "profiles" / "ncu_trace_summary.json"
     if prof.exists():
         try:
-            pj = json.loads(prof.read_text())
-            traffic = pj.get(a.precision, {}).get("dram_bytes_per_launch")
+            pj = json.loads(prof.read_text()).get(a.precision, {})
+            if "dram_bytes_per_step" in pj:
+                traffic = pj["dram_bytes_per_step"] * local_steps / a.steps
         except Exception:
             traffic = None
 
@@ -377,7 +399,8 @@ def run_b200(a, world, rank, local):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} hbm_gbs",
                          "bytes_per_step": bps, "kernel": f"trace_pool_{a.precision}",
-                         "kernel_ms_per_step": trace_ms / a.steps},
+                         "kernel_ms_per_step": trace_ms / a.steps,
+                         "traffic_source": "ncu dram bytes/step x steps per launch"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         line.update(extra)

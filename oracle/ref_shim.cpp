@@ -187,9 +187,13 @@ int ref_solve_cells(const ermc_grid_t* grid, const double* temperature,
         errors[w] = e.what();
       }
     };
+    // wall_time covers the per-cell trace loop only (threads start -> join),
+    // not the O(N) setup copies above, so small samples time the march.
+    auto t_trace = std::chrono::steady_clock::now();
     std::vector<std::thread> pool;
     for (int w = 0; w < nt; ++w) pool.emplace_back(work, w);
     for (auto& t : pool) t.join();
+    t0 = t_trace;
     for (auto& e : errors)
       if (!e.empty()) throw ermc::Error(e);
     for (int l = 0; l < cfg.n_levels; ++l) {

@@ -176,10 +176,11 @@ struct Timing {
 // Scheduling knobs (defaults tuned on B200; ERMC_* environment variables
 // override them for experiments — they never change results).
 struct Tune {
-  int inner_steps = 4;
-  int refill = 4;
-  int fp64_min_blocks = 4;
+  int inner_steps = 8;
+  int refill = 8;
+  int fp64_min_blocks = 5;
   int fp32_min_blocks = 6;
+  int pipeline = 0;
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -192,6 +193,7 @@ const Tune& tune() {
     x.refill = std::max(1, std::min(32, env_int("ERMC_REFILL", x.refill)));
     x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
+    x.pipeline = env_int("ERMC_PIPELINE", x.pipeline);
     return x;
   }();
   return t;
@@ -516,6 +518,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.rays = c.rays_per_cell;
   P.refill_threshold = tune().refill;
   P.inner_steps = tune().inner_steps;
+  P.pipeline = tune().pipeline;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;

@@ -188,7 +188,8 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         if (st == kDone) {
           const double q = tr.finish(P);
           if (isfinite(q) && tr.finite_state()) {
-            P.q_ray[static_cast<uint64_t>(slot_ray) * P.n_cells + slot_cell] = q;
+            // streaming store: keep the L2 for the temperature field
+            __stcs(P.q_ray + static_cast<uint64_t>(slot_ray) * P.n_cells + slot_cell, q);
             if (kMulti) {
               for (int l = 0; l < tr.level(); ++l)
                 atomicAdd(&s_steps[l],

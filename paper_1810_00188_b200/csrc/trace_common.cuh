@@ -80,6 +80,7 @@ struct TraceParams {
   // ---- work decomposition ----
   int32_t refill_threshold;  // idle lanes before a warp regenerates rays
   int32_t inner_steps;       // march steps between two pool checks
+  int32_t pipeline;          // 1: walker/integrator pipelined tracer
   int64_t cell_base;         // first global linear cell of this chunk
   int64_t n_cells;           // cells in this chunk
   uint64_t n_work;           // n_cells * rays (ray work items)

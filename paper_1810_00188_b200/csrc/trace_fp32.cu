@@ -305,6 +305,162 @@ struct Fp32Tracer {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
+// Pipelined single-level tracer. The geometry walker runs one step ahead
+// of the integrator: in iteration k it (L) finishes the DDA of step k+1,
+// looks up the table record of that step's cell (its T was fetched in
+// iteration k-1) and fetches T of the cell after it; then (M) it integrates
+// step k with the record fetched in iteration k-1. Both dependent gathers
+// get a full iteration of latency slack. A wall crossing parks the walker
+// until the integrator has decided between absorption and reflection.
+struct Fp32Pipe : Fp32Tracer {
+  float tw;        // T of the walker's cell (fetched one iteration ahead)
+  bool w_ok;       // walker active (false while parked at a wall)
+  bool e_ok;       // an entry is waiting for the integrator
+  float e_ds, e_f, e_t;
+  float4 e_v;
+  int e_fl;        // 0: interior/periodic exit, 1 + face: wall after this step
+
+  __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
+                                      uint32_t ray) {
+    const int e = Fp32Tracer::init(P, cell, ray);
+    tw = t_cur;
+    w_ok = true;
+    e_ok = false;
+    return e;
+  }
+
+  __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
+    const LevelDesc& L = P.lv[0];
+    // ---- L: walker step + table lookup of the step it produces
+    bool n_ok = false;
+    float n_ds = 0.0f, n_f = 0.0f, n_t = 0.0f;
+    float4 n_v = make_float4(0.f, 0.f, 0.f, 0.f);
+    int n_fl = 0;
+    if (w_ok) {
+      int axis = 0;
+      float tmin = tn[0];
+      if (tn[1] < tmin) {
+        tmin = tn[1];
+        axis = 1;
+      }
+      if (tn[2] < tmin) {
+        tmin = tn[2];
+        axis = 2;
+      }
+      n_ds = fmaxf(tmin - s, 0.0f);
+      s = fmaxf(tmin, s);
+      const float u = fmaf(tw, P.inv_dt32, -P.t0_32 * P.inv_dt32);
+      const int lo = min(max(static_cast<int>(u), 0), P.n_temps - 2);
+      n_f = u - static_cast<float>(lo);
+      n_v = __ldg(row + lo);
+      n_t = tw;
+      n_ok = true;
+      int ia = 0, na = 0, sa = 0, stride = 1;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) {
+          sa = stp[a];
+          ia = idx[a] + sa;
+          na = L.n[a];
+          stride = a == 0 ? L.n[1] * L.n[2] : (a == 1 ? L.n[2] : 1);
+          tn[a] += td[a];
+        }
+      if (ia >= 0 && ia < na) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (a == axis) idx[a] = ia;
+        lin += sa > 0 ? stride : -stride;
+        tw = __ldg(L.field32 + lin);
+      } else if (P.periodic[axis]) {
+        rebase();
+        const float ext = static_cast<float>(L.extent[axis]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (a == axis) {
+            if (ia < 0) {
+              idx[a] = na - 1;
+              p0[a] += ext;
+            } else {
+              idx[a] = 0;
+              p0[a] -= ext;
+            }
+          }
+        lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
+        tw = __ldg(L.field32 + lin);
+      } else {
+        n_fl = 1 + 2 * axis + (sa > 0 ? 1 : 0);
+        w_ok = false;  // parked at the wall until the integrator gets there
+      }
+    }
+    // ---- M: integrate the entry produced in the previous iteration
+    if (e_ok) {
+      if (tau <= P.tol32) return kDone;
+      if (steps_ >= max_steps) return kDone;
+      const float kappa = fmaf(e_f, e_v.y, e_v.x);
+      const float ib2n = fmaf(e_f, e_v.w, e_v.z);
+      const float alpha = absorb32(kappa * e_ds);
+      last_ib2n = ib2n;
+      const float ta = tau * alpha;
+      acc = fmaf(ta, ib2n - ib1n, acc);
+      tau -= ta;
+      ++steps_;
+      if (e_fl) {
+        // wall exchange (tracer.cpp:155-165)
+        const int face = e_fl - 1;
+        const int axis = face >> 1;
+        const bool at_hi = face & 1;
+        const float ew = static_cast<float>(P.wall_eps[face]);
+        const float ibw = __ldg(P.wall_ibn32 + face * P.n_bands + band);
+        const float tw_ = tau * ew;
+        acc = fmaf(tw_, ibw - ib1n, acc);
+        tau -= tw_;
+        if (tau <= P.tol32) return kDone;
+        // reflection (tracer.cpp:167-182): the walker is parked in this cell
+        rebase();
+        const float face_pos = static_cast<float>(
+            L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
+        float nd[3] = {dir[0], dir[1], dir[2]};
+        if (P.specular) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            if (a == axis) nd[a] = -nd[a];
+        } else {
+          const double r1 = draw_u(h_cell, ray_id, next_draw++);
+          const double r2 = draw_u(h_cell, ray_id, next_draw++);
+          const float sin_t = sqrtf(static_cast<float>(r1));
+          const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
+          float sp, cp;
+          sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
+          const int t1 = axis == 2 ? 0 : axis + 1;
+          const int t2 = axis == 0 ? 2 : axis - 1;
+          const float inward = at_hi ? -1.0f : 1.0f;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (a == axis) nd[a] = inward * cos_t;
+            if (a == t1) nd[a] = sin_t * cp;
+            if (a == t2) nd[a] = sin_t * sp;
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (a == axis) p0[a] = face_pos;
+          dir[a] = nd[a];
+        }
+        setup(L);
+        tw = e_t;
+        w_ok = true;
+      }
+    }
+    e_ok = n_ok;
+    e_ds = n_ds;
+    e_f = n_f;
+    e_t = n_t;
+    e_v = n_v;
+    e_fl = n_fl;
+    return kContinue;
+  }
+};
+
 struct Fp32Single : Fp32Tracer {
   __device__ __forceinline__ int step(const TraceParams& P, int m) {
     return step_t<false>(P, m);
@@ -321,6 +477,8 @@ __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32(const __grid_constant__ TraceParams P) {
   if (kMulti)
     pool_kernel_body<Fp32Multi, true>(P);
+  else if (P.pipeline)
+    pool_kernel_body<Fp32Pipe, false>(P);
   else
     pool_kernel_body<Fp32Single, false>(P);
 }

@@ -396,9 +396,19 @@ __device__ __forceinline__ double div_rcp(double a, double b, double r) {
   return fma(e, r, q0);
 }
 
-// SpectralModel::lookup on the packed tables (uniform or not).
-__device__ __forceinline__ bool fast_lookup(const TraceParams& P, double T,
-                                            int& lo, double& frac) {
+// The reference's table index trunc((T - t0) / dt) with the IEEE division;
+// kept out of line so the common multiply path is not if-converted into it.
+__device__ __noinline__ int exact_index(double T, double t0, double dt) {
+  return static_cast<int>((T - t0) / dt);
+}
+
+// SpectralModel::lookup on the packed tables (uniform or not). The interval
+// record of the returned lo is loaded into *rec (issued together with the
+// temperature record so the two loads overlap).
+__device__ __forceinline__ bool fast_lookup(const TraceParams& P,
+                                            const double4* row, double T,
+                                            int& lo, double& frac,
+                                            double4& rec) {
   if (!(T >= P.t_first && T <= P.t_last)) return false;
   const int nt = P.n_temps;
   int l;
@@ -406,19 +416,18 @@ __device__ __forceinline__ bool fast_lookup(const TraceParams& P, double T,
     const double x = (T - P.t0) * P.inv_dt;
     const double xf = x - floor(x);
     if (xf < 1e-9 || xf > 1.0 - 1e-9)
-      l = static_cast<int>((T - P.t0) / P.dt);  // the reference's quotient
+      l = exact_index(T, P.t0, P.dt);
     else
       l = static_cast<int>(x);
     l = min(max(l, 0), nt - 2);
     double4 ti = ldg4(P.tint + l);
+    rec = ldg4(row + l);
     double f = div_rcp(T - ti.x, ti.y, ti.z);
-    if (f < 0.0 && l > 0) {
-      --l;
+    if ((f < 0.0 && l > 0) || (f > 1.0 && l < nt - 2)) {
+      // rounding put T in the neighbouring interval (spectral.cpp:159-168)
+      l += f < 0.0 ? -1 : 1;
       ti = ldg4(P.tint + l);
-      f = div_rcp(T - ti.x, ti.y, ti.z);
-    } else if (f > 1.0 && l < nt - 2) {
-      ++l;
-      ti = ldg4(P.tint + l);
+      rec = ldg4(row + l);
       f = div_rcp(T - ti.x, ti.y, ti.z);
     }
     lo = l;
@@ -437,6 +446,7 @@ __device__ __forceinline__ bool fast_lookup(const TraceParams& P, double T,
     const double4 ti = ldg4(P.tint + lo);
     frac = div_rcp(T - ti.x, ti.y, ti.z);
   }
+  rec = ldg4(row + lo);
   return true;
 }
 
@@ -488,11 +498,11 @@ struct Fp64Fast {
     const LevelDesc& L = P.lv[0];
     int lo;
     double frac;
-    if (!fast_lookup(P, t_cur, lo, frac)) {
+    double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
+    if (!fast_lookup(P, row, t_cur, lo, frac, v)) {
       err = kErrTableRange;
       return kFail;
     }
-    const double4 v = ldg4(row + lo);  // {k_lo, k_hi, ib_lo, ib_hi}
 
     int axis = 0;
     double ds = tn[0];
