@@ -923,3 +923,61 @@ int oracle_slab(double length, int profile, double tc, double kappa, double t_lo
   }
   return 0;
 }
+
+/* ------------------------------------------------------------ kernel check */
+/* C restatement of the fp64 lean kernel's expm1 (trace_fp64.cu,
+ * expm1_lean) so tests can bound its distance to glibc's expm1 (the
+ * reference's libm) on the CPU. Same operations, same fma() calls. */
+double oracle_expm1_lean(double x) {
+  static const double c[12] = {1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720,
+                               1.0 / 5040, 1.0 / 40320, 1.0 / 362880, 1.0 / 3628800,
+                               1.0 / 39916800, 1.0 / 479001600, 1.0 / 6227020800.0};
+  if (!(x >= -40.0 && x <= 0.5)) {
+    if (x < -40.0) return -1.0;
+    return expm1(x);
+  }
+  const double magic = 6755399441055744.0;
+  double t = fma(x, 1.4426950408889634074, magic);
+  double j = t - magic;
+  double r = fma(j, -6.93147180369123816490e-01, x);
+  r = fma(j, -1.90821492927058770002e-10, r);
+  double p = c[11];
+  for (int i = 10; i >= 0; --i) p = fma(p, r, c[i]);
+  double e = fma(r * r, p, r);
+  long long ji = (long long)j;
+  if (ji == 0) return e;
+  uint64_t bits = (uint64_t)(ji + 1023) << 52;
+  double sc;
+  memcpy(&sc, &bits, sizeof sc);
+  return fma(sc, e, sc - 1.0);
+}
+
+/* max |ulp| distance of oracle_expm1_lean to glibc expm1 over n stratified
+ * samples of the march's arguments x = -kappa ds in [-40, 0]. */
+double oracle_expm1_lean_max_ulp(long n, long* n_differ) {
+  uint64_t s = 7;
+  double worst = 0.0;
+  long differ = 0;
+  for (long i = 0; i < n; ++i) {
+    s ^= s << 13;
+    s ^= s >> 7;
+    s ^= s << 17;
+    double u = (double)(s >> 11) * 0x1p-53, x;
+    switch (i % 5) {
+      case 0: x = -u * 40; break;
+      case 1: x = -u * 2; break;
+      case 2: x = -u * 1e-3; break;
+      case 3: x = -u * 1e-8; break;
+      default: x = -exp(-u * 40); break;
+    }
+    double a = oracle_expm1_lean(x), b = expm1(x);
+    if (a != b) {
+      ++differ;
+      double ulp = nextafter(fabs(b), 1.0 / 0.0) - fabs(b);
+      double d = fabs(a - b) / ulp;
+      if (d > worst) worst = d;
+    }
+  }
+  if (n_differ) *n_differ = differ;
+  return worst;
+}

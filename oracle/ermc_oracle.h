@@ -63,6 +63,10 @@ int oracle_slab(double length, int profile, double t_const, double kappa,
                 const double* x, int nx, int refine, double* q, char* err,
                 size_t errlen);
 
+/* Restatement of the fp64 lean kernel's expm1 and its distance to glibc. */
+double oracle_expm1_lean(double x);
+double oracle_expm1_lean_max_ulp(long n, long* n_differ);
+
 double oracle_expint_e1(double x);
 double oracle_expint_e2(double x);
 double oracle_expint_e3(double x);

@@ -53,7 +53,10 @@ def lib() -> C.CDLL:
         L.oracle_slab.argtypes = [C.c_double, C.c_int, C.c_double, C.c_double, C.c_double,
                                   C.c_double, C.c_double, C.c_double, _d, C.c_int, C.c_int,
                                   _d, C.c_char_p, C.c_size_t]
-        for f in ("oracle_expint_e1", "oracle_expint_e2", "oracle_expint_e3"):
+        L.oracle_expm1_lean_max_ulp.restype = C.c_double
+        L.oracle_expm1_lean_max_ulp.argtypes = [C.c_long, C.POINTER(C.c_long)]
+        for f in ("oracle_expint_e1", "oracle_expint_e2", "oracle_expint_e3",
+                  "oracle_expm1_lean"):
             getattr(L, f).restype = C.c_double
             getattr(L, f).argtypes = [C.c_double]
         _lib = L
@@ -139,3 +142,8 @@ def slab(profile, t_const, kappa, wall_lo, wall_hi, xs, length=1.0, refine=1):
 
 def expint(order, x):
     return getattr(lib(), f"oracle_expint_e{order}")(x)
+
+
+def expm1_lean_max_ulp(n):
+    d = C.c_long()
+    return lib().oracle_expm1_lean_max_ulp(n, C.byref(d)), d.value

@@ -176,11 +176,11 @@ struct Timing {
 // Scheduling knobs (defaults tuned on B200; ERMC_* environment variables
 // override them for experiments — they never change results).
 struct Tune {
-  int inner_steps = 8;
+  int inner_steps = 16;
   int refill = 8;
-  int fp64_min_blocks = 5;
+  int fp64_min_blocks = 6;
   int fp32_min_blocks = 6;
-  int pipeline = 0;
+  int lean = 1;
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -193,7 +193,7 @@ const Tune& tune() {
     x.refill = std::max(1, std::min(32, env_int("ERMC_REFILL", x.refill)));
     x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
-    x.pipeline = env_int("ERMC_PIPELINE", x.pipeline);
+    x.lean = env_int("ERMC_LEAN", x.lean);
     return x;
   }();
   return t;
@@ -475,7 +475,10 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   ermc_dev::TraceParams& P = pr.P;
   std::memset(&P, 0, sizeof(P));
   P.n_levels = c.n_levels;
-  for (int a = 0; a < 3; ++a) P.periodic[a] = b.kind[a] == ERMC_AXIS_PERIODIC;
+  for (int a = 0; a < 3; ++a) {
+    P.periodic[a] = b.kind[a] == ERMC_AXIS_PERIODIC;
+    P.periodic_mask |= P.periodic[a] << a;
+  }
   for (int l = 0; l < c.n_levels; ++l) {
     const ermc_grid_t& g = grids[l];
     ermc_dev::LevelDesc& L = P.lv[l];
@@ -518,7 +521,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.rays = c.rays_per_cell;
   P.refill_threshold = tune().refill;
   P.inner_steps = tune().inner_steps;
-  P.pipeline = tune().pipeline;
+  P.lean = tune().lean;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;
@@ -741,6 +744,7 @@ void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
   P.iv32 = s->d_iv32.p;
   P.inv_dt32 = static_cast<float>(1.0 / v.dt);
   P.t0_32 = static_cast<float>(v.t0);
+  P.u0_32 = -P.t0_32 * P.inv_dt32;
 }
 
 template <typename F>

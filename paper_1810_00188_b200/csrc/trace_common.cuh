@@ -39,6 +39,7 @@ struct TraceParams {
   // ---- geometry ----
   int32_t n_levels;
   int32_t periodic[3];
+  int32_t periodic_mask;     // bit a set when axis a is periodic
   LevelDesc lv[kMaxLevels];
   double wall_eps[6];        // face = 2*axis + (hi ? 1 : 0)
   const double* wall_ib;     // [6][n_bands] interp_ib(band, T_wall) or 0
@@ -67,6 +68,7 @@ struct TraceParams {
   float inv_dt32;            // 1/dt for the fp32 lookup (uniform grids only)
   float t0_32;
   float tol32;               // tolerance as float
+  float u0_32;               // -t0 / dt as float (table coordinate offset)
 
   // ---- march options (TraceOptions, tracer.hpp:26-30) ----
   double qe;                 // 4 kappa_p(T_max) sigma T_max^4 / R (solver.cpp:92-93)
@@ -80,7 +82,7 @@ struct TraceParams {
   // ---- work decomposition ----
   int32_t refill_threshold;  // idle lanes before a warp regenerates rays
   int32_t inner_steps;       // march steps between two pool checks
-  int32_t pipeline;          // 1: walker/integrator pipelined tracer
+  int32_t lean;              // fp64: 1 = lean tracer (per-axis records in smem)
   int64_t cell_base;         // first global linear cell of this chunk
   int64_t n_cells;           // cells in this chunk
   uint64_t n_work;           // n_cells * rays (ray work items)

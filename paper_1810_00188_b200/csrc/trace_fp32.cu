@@ -305,182 +305,227 @@ struct Fp32Tracer {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-// Pipelined single-level tracer. The geometry walker runs one step ahead
-// of the integrator: in iteration k it (L) finishes the DDA of step k+1,
-// looks up the table record of that step's cell (its T was fetched in
-// iteration k-1) and fetches T of the cell after it; then (M) it integrates
-// step k with the record fetched in iteration k-1. Both dependent gathers
-// get a full iteration of latency slack. A wall crossing parks the walker
-// until the integrator has decided between absorption and reflection.
-struct Fp32Pipe : Fp32Tracer {
-  float tw;        // T of the walker's cell (fetched one iteration ahead)
-  bool w_ok;       // walker active (false while parked at a wall)
-  bool e_ok;       // an entry is waiting for the integrator
-  float e_ds, e_f, e_t;
-  float4 e_v;
-  int e_fl;        // 0: interior/periodic exit, 1 + face: wall after this step
+// Lean single-level tracer: the per-axis constants of the DDA live in a
+// per-thread shared-memory record indexed by the stepping axis,
+//   ax[a] = {t_delta (float bits), signed linear stride, cells left before
+//            the domain face, wrap delta (-stride * n) or the fixed index of
+//            a non-moving axis},
+// so one LDS.128 replaces the predicated per-axis selects and param-space
+// loads of a register-only DDA; `lin` carries the cell index.
+struct Fp32Lean {
+  float p0[3], dir[3], tn[3];
+  float s, tau, acc, ib1n, last_ib2n, t_cur;
+  double cq;
+  const float4* row;
+  int4* ax;  // &s_ax[0][threadIdx.x]; axis a at ax[a * kBlock32]
+  int lin, band, steps_;
+  uint32_t next_draw, ray_id;
+  uint64_t h_cell;
+  int err;
+
+  __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
+    const int4 r = ax[a * kBlock32];
+    if (dir[a] == 0.0f) return r.w;
+    return dir[a] > 0.0f ? L.n[a] - 1 - r.z : r.z;
+  }
+
+  __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx) {
+    const int stride[3] = {L.n[1] * L.n[2], L.n[2], 1};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float da = dir[a];
+      if (da == 0.0f) {
+        tn[a] = __int_as_float(0x7f800000);
+        ax[a * kBlock32] = make_int4(0x7f800000, 0, 0x7fffffff, idx[a]);
+        continue;
+      }
+      const float inv = 1.0f / da;
+      const bool pos = da > 0.0f;
+      const float face =
+          static_cast<float>(L.origin[a] + (idx[a] + (pos ? 1 : 0)) * L.d[a]);
+      tn[a] = (face - p0[a]) * inv;
+      const float td = static_cast<float>(L.d[a]) * fabsf(inv);
+      const int dl = pos ? stride[a] : -stride[a];
+      ax[a * kBlock32] = make_int4(__float_as_int(td), dl,
+                                   pos ? L.n[a] - 1 - idx[a] : idx[a], -dl * L.n[a]);
+    }
+    s = 0.0f;
+    lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
+  }
+
+  __device__ __forceinline__ void rebase() {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      p0[a] = fmaf(s, dir[a], p0[a]);
+      tn[a] -= s;
+    }
+    s = 0.0f;
+  }
 
   __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
                                       uint32_t ray) {
-    const int e = Fp32Tracer::init(P, cell, ray);
-    tw = t_cur;
-    w_ok = true;
-    e_ok = false;
-    return e;
+    extern __shared__ int4 s_dyn[];
+    ax = s_dyn + threadIdx.x;
+    Fp32Tracer base;
+    const int e = base.init(P, cell, ray);
+    if (e != kErrNone) return e;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      p0[a] = base.p0[a];
+      dir[a] = base.dir[a];
+    }
+    tau = 1.0f;
+    acc = 0.0f;
+    ib1n = base.ib1n;
+    last_ib2n = base.ib1n;
+    cq = base.cq;
+    row = base.row;
+    band = base.band;
+    steps_ = 0;
+    next_draw = base.next_draw;
+    ray_id = ray;
+    h_cell = base.h_cell;
+    t_cur = base.t_cur;
+    setup(P.lv[0], base.idx);
+    return kErrNone;
   }
 
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
+    if (tau <= P.tol32) return kDone;
+    if (steps_ >= max_steps) return kDone;
     const LevelDesc& L = P.lv[0];
-    // ---- L: walker step + table lookup of the step it produces
-    bool n_ok = false;
-    float n_ds = 0.0f, n_f = 0.0f, n_t = 0.0f;
-    float4 n_v = make_float4(0.f, 0.f, 0.f, 0.f);
-    int n_fl = 0;
-    if (w_ok) {
-      int axis = 0;
-      float tmin = tn[0];
-      if (tn[1] < tmin) {
-        tmin = tn[1];
-        axis = 1;
-      }
-      if (tn[2] < tmin) {
-        tmin = tn[2];
-        axis = 2;
-      }
-      n_ds = fmaxf(tmin - s, 0.0f);
-      s = fmaxf(tmin, s);
-      const float u = fmaf(tw, P.inv_dt32, -P.t0_32 * P.inv_dt32);
-      const int lo = min(max(static_cast<int>(u), 0), P.n_temps - 2);
-      n_f = u - static_cast<float>(lo);
-      n_v = __ldg(row + lo);
-      n_t = tw;
-      n_ok = true;
-      int ia = 0, na = 0, sa = 0, stride = 1;
+    // table record of the current cell (its T arrived during the last step)
+    const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
+    const int lo = min(static_cast<int>(u), P.n_temps - 2);
+    const float f = u - static_cast<float>(lo);
+    const float4 v = __ldg(row + lo);
+
+    int axis = 0;
+    float tmin = tn[0];
+    if (tn[1] < tmin) {
+      tmin = tn[1];
+      axis = 1;
+    }
+    if (tn[2] < tmin) {
+      tmin = tn[2];
+      axis = 2;
+    }
+    const float ds = fmaxf(tmin - s, 0.0f);
+    s = fmaxf(tmin, s);
+
+    int4* rp = ax + axis * kBlock32;
+    const int4 r = *rp;
+    const float td = __int_as_float(r.x);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) tn[a] += td;
+    const int left = r.z - 1;
+    const bool inside = left >= 0;
+    const int nlin = lin + r.y + (inside ? 0 : r.w);  // periodic image if outside
+    float t_next = t_cur;
+    if (inside || P.periodic[axis]) t_next = __ldg(L.field32 + nlin);
+
+    const float kappa = fmaf(f, v.y, v.x);
+    const float ib2n = fmaf(f, v.w, v.z);
+    const float alpha = absorb32(kappa * ds);
+    last_ib2n = ib2n;
+    const float ta = tau * alpha;
+    acc = fmaf(ta, ib2n - ib1n, acc);
+    tau -= ta;
+    ++steps_;
+
+    if (inside) {
+      rp->z = left;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    if (P.periodic[axis]) {
+      rp->z = L.n[axis] - 1;
+      rebase();
+      const float ext = static_cast<float>(L.extent[axis]);
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        if (a == axis) {
-          sa = stp[a];
-          ia = idx[a] + sa;
-          na = L.n[a];
-          stride = a == 0 ? L.n[1] * L.n[2] : (a == 1 ? L.n[2] : 1);
-          tn[a] += td[a];
-        }
-      if (ia >= 0 && ia < na) {
+        if (a == axis) p0[a] += r.y > 0 ? -ext : ext;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    // wall exchange (tracer.cpp:155-165); the ray stays in its cell
+    const bool at_hi = r.y > 0;
+    const int face = 2 * axis + (at_hi ? 1 : 0);
+    const float ew = static_cast<float>(P.wall_eps[face]);
+    const float ibw = __ldg(P.wall_ibn32 + face * P.n_bands + band);
+    const float tw = tau * ew;
+    acc = fmaf(tw, ibw - ib1n, acc);
+    tau -= tw;
+    if (tau <= P.tol32) return kDone;
+    // reflection (tracer.cpp:167-182)
+    int idx[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-          if (a == axis) idx[a] = ia;
-        lin += sa > 0 ? stride : -stride;
-        tw = __ldg(L.field32 + lin);
-      } else if (P.periodic[axis]) {
-        rebase();
-        const float ext = static_cast<float>(L.extent[axis]);
+    for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);  // rp->z still 0: the boundary cell
+    rebase();
+    const float face_pos =
+        static_cast<float>(L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
+    float nd[3] = {dir[0], dir[1], dir[2]};
+    if (P.specular) {
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-          if (a == axis) {
-            if (ia < 0) {
-              idx[a] = na - 1;
-              p0[a] += ext;
-            } else {
-              idx[a] = 0;
-              p0[a] -= ext;
-            }
-          }
-        lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
-        tw = __ldg(L.field32 + lin);
-      } else {
-        n_fl = 1 + 2 * axis + (sa > 0 ? 1 : 0);
-        w_ok = false;  // parked at the wall until the integrator gets there
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) nd[a] = -nd[a];
+    } else {
+      const double r1 = draw_u(h_cell, ray_id, next_draw++);
+      const double r2 = draw_u(h_cell, ray_id, next_draw++);
+      const float sin_t = sqrtf(static_cast<float>(r1));
+      const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
+      float sp, cp;
+      sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
+      const int t1 = axis == 2 ? 0 : axis + 1;
+      const int t2 = axis == 0 ? 2 : axis - 1;
+      const float inward = at_hi ? -1.0f : 1.0f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a == axis) nd[a] = inward * cos_t;
+        if (a == t1) nd[a] = sin_t * cp;
+        if (a == t2) nd[a] = sin_t * sp;
       }
     }
-    // ---- M: integrate the entry produced in the previous iteration
-    if (e_ok) {
-      if (tau <= P.tol32) return kDone;
-      if (steps_ >= max_steps) return kDone;
-      const float kappa = fmaf(e_f, e_v.y, e_v.x);
-      const float ib2n = fmaf(e_f, e_v.w, e_v.z);
-      const float alpha = absorb32(kappa * e_ds);
-      last_ib2n = ib2n;
-      const float ta = tau * alpha;
-      acc = fmaf(ta, ib2n - ib1n, acc);
-      tau -= ta;
-      ++steps_;
-      if (e_fl) {
-        // wall exchange (tracer.cpp:155-165)
-        const int face = e_fl - 1;
-        const int axis = face >> 1;
-        const bool at_hi = face & 1;
-        const float ew = static_cast<float>(P.wall_eps[face]);
-        const float ibw = __ldg(P.wall_ibn32 + face * P.n_bands + band);
-        const float tw_ = tau * ew;
-        acc = fmaf(tw_, ibw - ib1n, acc);
-        tau -= tw_;
-        if (tau <= P.tol32) return kDone;
-        // reflection (tracer.cpp:167-182): the walker is parked in this cell
-        rebase();
-        const float face_pos = static_cast<float>(
-            L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
-        float nd[3] = {dir[0], dir[1], dir[2]};
-        if (P.specular) {
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
-            if (a == axis) nd[a] = -nd[a];
-        } else {
-          const double r1 = draw_u(h_cell, ray_id, next_draw++);
-          const double r2 = draw_u(h_cell, ray_id, next_draw++);
-          const float sin_t = sqrtf(static_cast<float>(r1));
-          const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
-          float sp, cp;
-          sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
-          const int t1 = axis == 2 ? 0 : axis + 1;
-          const int t2 = axis == 0 ? 2 : axis - 1;
-          const float inward = at_hi ? -1.0f : 1.0f;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            if (a == axis) nd[a] = inward * cos_t;
-            if (a == t1) nd[a] = sin_t * cp;
-            if (a == t2) nd[a] = sin_t * sp;
-          }
-        }
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          if (a == axis) p0[a] = face_pos;
-          dir[a] = nd[a];
-        }
-        setup(L);
-        tw = e_t;
-        w_ok = true;
-      }
+    for (int a = 0; a < 3; ++a) {
+      if (a == axis) p0[a] = face_pos;
+      dir[a] = nd[a];
     }
-    e_ok = n_ok;
-    e_ds = n_ds;
-    e_f = n_f;
-    e_t = n_t;
-    e_v = n_v;
-    e_fl = n_fl;
+    setup(L, idx);
     return kContinue;
   }
+
+  __device__ __forceinline__ double finish(const TraceParams&) const {
+    return cq * static_cast<double>(fmaf(tau, last_ib2n - ib1n, acc));
+  }
+  __device__ __forceinline__ bool finite_state() const {
+    return isfinite(tau) && isfinite(acc);
+  }
+  __device__ __forceinline__ int level() const { return 0; }
+  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-struct Fp32Single : Fp32Tracer {
-  __device__ __forceinline__ int step(const TraceParams& P, int m) {
-    return step_t<false>(P, m);
-  }
-};
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kBlock32, kMinBlocks)
+    trace_pool_fp32_lean(const __grid_constant__ TraceParams P) {
+  pool_kernel_body<Fp32Lean, false>(P);
+}
+
 struct Fp32Multi : Fp32Tracer {
   __device__ __forceinline__ int step(const TraceParams& P, int m) {
     return step_t<true>(P, m);
   }
 };
 
-template <bool kMulti, int kMinBlocks>
+// Multigrid variant (levels > 1): the register-DDA tracer with demotion.
+template <int kMinBlocks>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32(const __grid_constant__ TraceParams P) {
-  if (kMulti)
-    pool_kernel_body<Fp32Multi, true>(P);
-  else if (P.pipeline)
-    pool_kernel_body<Fp32Pipe, false>(P);
-  else
-    pool_kernel_body<Fp32Single, false>(P);
+  pool_kernel_body<Fp32Multi, true>(P);
 }
 
 // {k_lo, k_hi - k_lo, ibn_lo, ibn_hi - ibn_lo} per (band, g, interval),
@@ -517,22 +562,27 @@ int trace_fp32_block() { return kBlock32; }
 
 namespace {
 using TraceFn32 = void (*)(TraceParams);
-TraceFn32 fp32_kernel(bool multi, int min_blocks) {
-  if (multi) return min_blocks >= 8 ? trace_pool_fp32<true, 8> : trace_pool_fp32<true, 6>;
-  return min_blocks >= 8 ? trace_pool_fp32<false, 8> : trace_pool_fp32<false, 6>;
+bool fp32_lean(const TraceParams& P) { return P.n_levels == 1; }
+size_t fp32_smem(const TraceParams& P) {
+  return fp32_lean(P) ? 3 * kBlock32 * sizeof(int4) : 0;
+}
+TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
+  if (fp32_lean(P))
+    return min_blocks >= 8 ? trace_pool_fp32_lean<8> : trace_pool_fp32_lean<6>;
+  return min_blocks >= 8 ? trace_pool_fp32<8> : trace_pool_fp32<6>;
 }
 }  // namespace
 
 int trace_fp32_blocks_per_sm(const TraceParams& P, int min_blocks) {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &nb, fp32_kernel(P.n_levels > 1, min_blocks), kBlock32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fp32_kernel(P, min_blocks), kBlock32,
+                                                fp32_smem(P));
   return nb;
 }
 
 cudaError_t launch_trace_fp32(const TraceParams& P, int grid, int min_blocks,
                               cudaStream_t stream) {
-  fp32_kernel(P.n_levels > 1, min_blocks)<<<grid, kBlock32, 0, stream>>>(P);
+  fp32_kernel(P, min_blocks)<<<grid, kBlock32, fp32_smem(P), stream>>>(P);
   return cudaGetLastError();
 }
 

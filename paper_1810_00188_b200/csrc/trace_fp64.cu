@@ -29,6 +29,7 @@ namespace ermc_dev {
 namespace {
 
 constexpr double kPiD = kPiDev;
+constexpr int kBlock = 128;
 constexpr unsigned kFull = kFullMask;
 
 // SpectralModel::lookup (reference spectral.cpp:148-177). Returns false when
@@ -646,6 +647,239 @@ struct Fp64Fast {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
+// ---------------------------------------------------------------------------
+// expm1 for the lean tracer: x = j ln2 + r with |r| <= ln2/2 (Cody-Waite with
+// fdlibm's split of ln2), e^r - 1 = r + r^2 (1/2 + r/6 + ... + r^11/13!)
+// (Taylor to degree 13: truncation < 0.1 ulp), expm1(x) = 2^j (e^r - 1) +
+// (2^j - 1). Coefficients come from the constant bank (no per-use 64-bit
+// immediates). Within 1 ulp of glibc's expm1 on 5e7 samples of the march's
+// argument range (tests/test_oracle.py::test_expm1_restatement), the same
+// accuracy class as libdevice's.
+__constant__ double kEm1Coef[12] = {
+    1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040,
+    1.0 / 40320, 1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800,
+    1.0 / 479001600, 1.0 / 6227020800.0};
+
+__device__ __forceinline__ double expm1_lean(double x) {
+  if (!(x >= -40.0 && x <= 0.5)) {
+    if (x < -40.0) return -1.0;  // |expm1(x) + 1| < 2^-57
+    return expm1(x);             // NaN, positive arguments: libdevice
+  }
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(x, 1.4426950408889634074, magic);
+  const double j = t - magic;
+  double r = fma(j, -6.93147180369123816490e-01, x);
+  r = fma(j, -1.90821492927058770002e-10, r);
+  double p = kEm1Coef[11];
+#pragma unroll
+  for (int i = 10; i >= 0; --i) p = fma(p, r, kEm1Coef[i]);
+  const double e = fma(r * r, p, r);
+  const int ji = __double2loint(t);
+  if (ji == 0) return e;
+  const double sc = __hiloint2double((ji + 1023) << 20, 0);
+  return fma(sc, e, sc - 1.0);
+}
+
+// Lean single-level fp64 tracer: Fp64Fast's arithmetic (hence the
+// reference's) with the per-axis DDA constants in a per-thread shared-memory
+// record indexed by the stepping axis:
+//   ax[a] = {t_delta (lo, hi words), signed linear stride, cells left before
+//            the domain face (or the fixed index of a non-moving axis)}.
+struct Fp64Lean {
+  double pos[3], dir[3], tn[3];
+  double tau, q, last_ib2, ib1, rib1, pref, t_cur;
+  const double4* row;
+  int4* ax;
+  int lin, band, steps_;
+  uint32_t next_draw, ray_id;
+  uint64_t h_cell;
+  int err;
+
+  __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
+    const int left = ax[a * kBlock].w;
+    if (dir[a] == 0.0) return left;
+    return dir[a] > 0.0 ? L.n[a] - 1 - left : left;
+  }
+
+  // Dda::setup (tracer.cpp:17-38) + the per-axis records.
+  __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx) {
+    const int stride[3] = {L.n[1] * L.n[2], L.n[2], 1};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double da = dir[a];
+      if (da == 0.0) {
+        tn[a] = __longlong_as_double(0x7ff0000000000000LL);
+        ax[a * kBlock] = make_int4(0, 0x7ff00000, 0, idx[a]);
+        continue;
+      }
+      const bool pos_dir = da > 0.0;
+      const int face_idx = idx[a] + (pos_dir ? 1 : 0);
+      const double face = L.origin[a] + face_idx * L.d[a];
+      tn[a] = (face - pos[a]) / da;
+      const double td = L.d[a] / fabs(da);
+      ax[a * kBlock] = make_int4(__double2loint(td), __double2hiint(td),
+                                 pos_dir ? stride[a] : -stride[a],
+                                 pos_dir ? L.n[a] - 1 - idx[a] : idx[a]);
+    }
+    lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
+  }
+
+  __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
+                                      uint32_t ray) {
+    extern __shared__ int4 s_dyn[];
+    ax = s_dyn + threadIdx.x;
+    Ray r;
+    const int e = init_ray(P, cell, ray, r, nullptr);
+    if (e != kErrNone) return e;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      pos[a] = r.pos[a];
+      dir[a] = r.dir[a];
+    }
+    tau = 1.0;
+    q = 0.0;
+    ib1 = r.ib1;
+    last_ib2 = r.ib1;
+    rib1 = 1.0 / r.ib1;
+    pref = r.pref;
+    band = r.band;
+    const int64_t ng = (r.krow - P.k) / P.n_temps;
+    row = P.iv64 + ng * (P.n_temps - 1);
+    steps_ = 0;
+    next_draw = r.next_draw;
+    ray_id = ray;
+    h_cell = r.h_cell;
+    t_cur = __ldg(P.lv[0].field + cell);
+    setup(P.lv[0], r.idx);
+    return kErrNone;
+  }
+
+  __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
+    if (tau <= P.tol) return kDone;
+    if (steps_ >= max_steps) return kDone;
+    const LevelDesc& L = P.lv[0];
+    int lo;
+    double frac;
+    double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
+    if (!fast_lookup(P, row, t_cur, lo, frac, v)) {
+      err = kErrTableRange;
+      return kFail;
+    }
+    int axis = 0;
+    double ds = tn[0];
+    if (tn[1] < ds) {
+      ds = tn[1];
+      axis = 1;
+    }
+    if (tn[2] < ds) {
+      ds = tn[2];
+      axis = 2;
+    }
+    if (ds < 0.0) ds = 0.0;
+
+    int4* rp = ax + axis * kBlock;
+    const int4 rec = *rp;
+    const double td = __hiloint2double(rec.y, rec.x);
+    const int left = rec.w - 1;
+    const bool inside = left >= 0;
+    const bool periodic = (P.periodic_mask >> axis) & 1;
+    int nlin = lin + rec.z;
+    if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
+    double t_next = t_cur;
+    if (inside || periodic) t_next = __ldg(L.field + nlin);
+
+    const double kappa = frac == 0.0 ? v.x : v.x + frac * (v.y - v.x);
+    const double ib2 = frac == 0.0 ? v.z : v.z + frac * (v.w - v.z);
+    const double alpha = -expm1_lean(-kappa * ds);
+    last_ib2 = ib2;
+    q += P.qe * tau * alpha * div_rcp(ib2 - ib1, ib1, rib1) * pref;
+    tau *= 1.0 - alpha;
+
+    const double advance = ds + L.eps;
+    pos[0] += advance * dir[0];
+    pos[1] += advance * dir[1];
+    pos[2] += advance * dir[2];
+    tn[0] -= advance;
+    tn[1] -= advance;
+    tn[2] -= advance;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) tn[a] += td;
+    ++steps_;
+
+    if (inside) {
+      rp->w = left;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    if (periodic) {
+      rp->w = L.n[axis] - 1;
+      const double ext = L.extent[axis];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) pos[a] += rec.z > 0 ? -ext : ext;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    // Wall exchange, absorption or reflection (tracer.cpp:155-184); the ray
+    // stays in its boundary cell (its record still says 0 cells left).
+    const bool at_hi = rec.z > 0;
+    const int face = 2 * axis + (at_hi ? 1 : 0);
+    const double ew = P.wall_eps[face];
+    const double ib_w = __ldg(P.wall_ib + face * P.n_bands + band);
+    q += P.qe * tau * ew * div_rcp(ib_w - ib1, ib1, rib1) * pref;
+    tau *= 1.0 - ew;
+    if (tau <= P.tol) return kDone;
+    int idx[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);
+    const double face_pos = L.origin[axis] + (at_hi ? L.extent[axis] : 0.0);
+    const int inward = at_hi ? -1 : 1;
+    double nd[3] = {dir[0], dir[1], dir[2]};
+    if (P.specular) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) nd[a] = -nd[a];
+    } else {
+      const double r1 = draw_u(h_cell, ray_id, next_draw++);
+      const double r2 = draw_u(h_cell, ray_id, next_draw++);
+      const double sin_t = sqrt(r1);
+      const double cos_t = sqrt(1.0 - r1);
+      const double phi = 2.0 * kPiD * r2;
+      double sp, cp;
+      sincos(phi, &sp, &cp);
+      const int t1 = axis == 2 ? 0 : axis + 1;
+      const int t2 = axis == 0 ? 2 : axis - 1;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a == axis) nd[a] = inward * cos_t;
+        if (a == t1) nd[a] = sin_t * cp;
+        if (a == t2) nd[a] = sin_t * sp;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a == axis) pos[a] = face_pos;
+      dir[a] = nd[a];
+    }
+    pos[0] += L.eps * dir[0];
+    pos[1] += L.eps * dir[1];
+    pos[2] += L.eps * dir[2];
+    setup(L, idx);
+    return kContinue;
+  }
+
+  __device__ __forceinline__ double finish(const TraceParams& P) const {
+    return q + P.qe * tau * div_rcp(last_ib2 - ib1, ib1, rib1) * pref;
+  }
+  __device__ __forceinline__ bool finite_state() const { return isfinite(tau); }
+  __device__ __forceinline__ int level() const { return 0; }
+  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int steps() const { return steps_; }
+};
+
 struct Fp64Tracer {
   Ray r;
   int err;
@@ -678,7 +912,6 @@ struct Fp64Multi : Fp64Tracer {
   }
 };
 
-constexpr int kBlock = 128;
 
 // K1: persistent ray-pool trace over the chunk's (cell, ray) work items.
 // kMulti = false: the fast single-level tracer; true: the reference-order
@@ -691,6 +924,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     pool_kernel_body<Fp64Multi, true>(P);
   else
     pool_kernel_body<Fp64Fast, false>(P);
+}
+
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+    trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
+  pool_kernel_body<Fp64Lean, false>(P);
 }
 
 // Debug/test kernel: one thread traces one explicit ray with full
@@ -891,6 +1130,17 @@ int trace_fp64_block() { return kBlock; }
 namespace {
 // Kernel variant by (path, min blocks per SM); 4 or 5 blocks of 128 threads.
 using TraceFn = void (*)(TraceParams);
+bool lean_path(const TraceParams& P) {
+  return P.n_levels == 1 && P.n_temps >= 2 && P.lean &&
+         P.lv[0].n[0] * static_cast<int64_t>(P.lv[0].n[1]) * P.lv[0].n[2] < (1LL << 31);
+}
+size_t fp64_smem(const TraceParams& P) { return lean_path(P) ? 3 * kBlock * sizeof(int4) : 0; }
+TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
+  if (lean_path(P))
+    return min_blocks >= 6 ? trace_pool_fp64_lean<6>
+                           : (min_blocks >= 5 ? trace_pool_fp64_lean<5> : trace_pool_fp64_lean<4>);
+  return nullptr;
+}
 TraceFn fp64_kernel(bool multi, int min_blocks) {
   if (multi) return min_blocks >= 5 ? trace_pool_fp64<true, 5> : trace_pool_fp64<true, 4>;
   return min_blocks >= 5 ? trace_pool_fp64<false, 5> : trace_pool_fp64<false, 4>;
@@ -903,14 +1153,17 @@ bool fp64_fast_path(const TraceParams& P) {
 
 int trace_fp64_blocks_per_sm(const TraceParams& P, int min_blocks) {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &nb, fp64_kernel(!fp64_fast_path(P), min_blocks), kBlock, 0);
+  TraceFn k = fp64_kernel_p(P, min_blocks);
+  if (!k) k = fp64_kernel(!fp64_fast_path(P), min_blocks);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kBlock, fp64_smem(P));
   return nb;
 }
 
 cudaError_t launch_trace_fp64(const TraceParams& P, int grid, int min_blocks,
                               cudaStream_t stream) {
-  fp64_kernel(!fp64_fast_path(P), min_blocks)<<<grid, kBlock, 0, stream>>>(P);
+  TraceFn k = fp64_kernel_p(P, min_blocks);
+  if (!k) k = fp64_kernel(!fp64_fast_path(P), min_blocks);
+  k<<<grid, kBlock, fp64_smem(P), stream>>>(P);
   return cudaGetLastError();
 }
 
