@@ -110,63 +110,62 @@ __device__ __forceinline__ void raise_error(const TraceParams& P, uint64_t key,
 template <class Tracer, bool kMulti>
 __device__ __forceinline__ void run_pool(const TraceParams& P,
                                          unsigned long long* s_steps) {
-  constexpr uint64_t kBatch = 128;
+  // Work ids are 32-bit: the host keeps every chunk below 2^31 items.
+  constexpr uint32_t kBatch = 128;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned lt_mask = (1u << lane) - 1u;
   const uint32_t rays = static_cast<uint32_t>(P.rays);
-  const uint64_t n_work = P.n_work;
+  const uint32_t n_work = static_cast<uint32_t>(P.n_work);
   const int max_steps = static_cast<int>(
       P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL);
 
   Tracer tr;
   bool active = false;
-  uint32_t slot_cell = 0, slot_ray = 0;
-  uint64_t my_work = 0;
-  uint64_t pool_next = 0, pool_end = 0;
+  uint32_t my_work = 0;
+  uint32_t pool_next = 0, pool_end = 0;
   bool exhausted = false;
   unsigned long long my_steps = 0;
 
   while (true) {
     const unsigned idle = __ballot_sync(kFullMask, !active);
-    const int n_idle = __popc(idle);
+    const uint32_t n_idle = __popc(idle);
     const bool can_get = pool_next < pool_end || !exhausted;
-    if (can_get && (n_idle >= P.refill_threshold || idle == kFullMask)) {
-      const uint64_t avail = pool_end - pool_next;
-      uint64_t nb = 0, nb_end = 0;
-      if (avail < static_cast<uint64_t>(n_idle) && !exhausted) {
+    if (can_get && (n_idle >= static_cast<uint32_t>(P.refill_threshold) ||
+                    idle == kFullMask)) {
+      const uint32_t avail = pool_end - pool_next;
+      uint32_t nb = 0, nb_end = 0;
+      if (avail < n_idle && !exhausted) {
         unsigned long long b = 0;
         if (lane == 0) b = atomicAdd(P.work_counter, kBatch);
         b = __shfl_sync(kFullMask, b, 0);
         if (b >= n_work) {
           exhausted = true;
         } else {
-          nb = b;
-          nb_end = b + kBatch < n_work ? b + kBatch : n_work;
+          nb = static_cast<uint32_t>(b);
+          nb_end = b + kBatch < n_work ? nb + kBatch : n_work;
         }
       }
       if (!active) {
-        const uint64_t rank = __popc(idle & lt_mask);
-        uint64_t w = ~0ull;
+        const uint32_t rank = __popc(idle & lt_mask);
+        uint32_t w = 0xffffffffu;
         if (rank < avail)
           w = pool_next + rank;
         else if (rank - avail < nb_end - nb)
           w = nb + (rank - avail);
-        if (w != ~0ull) {
-          const uint32_t w32 = static_cast<uint32_t>(w);
-          slot_cell = w32 / rays;
-          slot_ray = w32 - slot_cell * rays;
+        if (w != 0xffffffffu) {
+          const uint32_t cell = w / rays;
           my_work = w;
-          const int e = tr.init(P, P.cell_base + slot_cell, slot_ray);
+          const int e = tr.init(P, P.cell_base + cell, w - cell * rays);
           if (e == kErrNone)
             active = true;
           else
             raise_error(P, w, e);
         }
       }
-      if (avail >= static_cast<uint64_t>(n_idle)) {
+      if (avail >= n_idle) {
         pool_next += n_idle;
       } else if (nb_end > nb) {
-        uint64_t take = n_idle - avail;
+        uint32_t take = n_idle - avail;
         if (take > nb_end - nb) take = nb_end - nb;
         pool_next = nb + take;
         pool_end = nb_end;
@@ -188,8 +187,10 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         if (st == kDone) {
           const double q = tr.finish(P);
           if (isfinite(q) && tr.finite_state()) {
+            const uint32_t cell = my_work / rays;
+            const uint32_t ray = my_work - cell * rays;
             // streaming store: keep the L2 for the temperature field
-            __stcs(P.q_ray + static_cast<uint64_t>(slot_ray) * P.n_cells + slot_cell, q);
+            __stcs(P.q_ray + static_cast<uint64_t>(ray) * P.n_cells + cell, q);
             if (kMulti) {
               for (int l = 0; l < tr.level(); ++l)
                 atomicAdd(&s_steps[l],

@@ -685,14 +685,15 @@ __device__ __forceinline__ double expm1_lean(double x) {
 // record indexed by the stepping axis:
 //   ax[a] = {t_delta (lo, hi words), signed linear stride, cells left before
 //            the domain face (or the fixed index of a non-moving axis)}.
+// rec[3] = {band, next_draw, cell id, ray id}: state only walls touch.
+constexpr int kLeanRecs64 = 4;
+
 struct Fp64Lean {
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
-  const double4* row;
   int4* ax;
-  int lin, band, steps_;
-  uint32_t next_draw, ray_id;
-  uint64_t h_cell;
+  int row;  // first interval record of (band, g) in iv64
+  int lin, steps_;
   int err;
 
   __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
@@ -742,13 +743,11 @@ struct Fp64Lean {
     last_ib2 = r.ib1;
     rib1 = 1.0 / r.ib1;
     pref = r.pref;
-    band = r.band;
     const int64_t ng = (r.krow - P.k) / P.n_temps;
-    row = P.iv64 + ng * (P.n_temps - 1);
+    row = static_cast<int>(ng * (P.n_temps - 1));
     steps_ = 0;
-    next_draw = r.next_draw;
-    ray_id = ray;
-    h_cell = r.h_cell;
+    ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
+                               static_cast<int>(cell), static_cast<int>(ray));
     t_cur = __ldg(P.lv[0].field + cell);
     setup(P.lv[0], r.idx);
     return kErrNone;
@@ -761,7 +760,7 @@ struct Fp64Lean {
     int lo;
     double frac;
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
-    if (!fast_lookup(P, row, t_cur, lo, frac, v)) {
+    if (!fast_lookup(P, P.iv64 + row, t_cur, lo, frac, v)) {
       err = kErrTableRange;
       return kFail;
     }
@@ -827,8 +826,9 @@ struct Fp64Lean {
     // stays in its boundary cell (its record still says 0 cells left).
     const bool at_hi = rec.z > 0;
     const int face = 2 * axis + (at_hi ? 1 : 0);
+    const int4 r3 = ax[3 * kBlock];
     const double ew = P.wall_eps[face];
-    const double ib_w = __ldg(P.wall_ib + face * P.n_bands + band);
+    const double ib_w = __ldg(P.wall_ib + face * P.n_bands + r3.x);
     q += P.qe * tau * ew * div_rcp(ib_w - ib1, ib1, rib1) * pref;
     tau *= 1.0 - ew;
     if (tau <= P.tol) return kDone;
@@ -843,8 +843,12 @@ struct Fp64Lean {
       for (int a = 0; a < 3; ++a)
         if (a == axis) nd[a] = -nd[a];
     } else {
-      const double r1 = draw_u(h_cell, ray_id, next_draw++);
-      const double r2 = draw_u(h_cell, ray_id, next_draw++);
+      const uint64_t h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(r3.z));
+      const uint32_t ray_id = static_cast<uint32_t>(r3.w);
+      const uint32_t draw0 = static_cast<uint32_t>(r3.y);
+      const double r1 = draw_u(h_cell, ray_id, draw0);
+      const double r2 = draw_u(h_cell, ray_id, draw0 + 1);
+      ax[3 * kBlock].y = static_cast<int>(draw0 + 2);
       const double sin_t = sqrt(r1);
       const double cos_t = sqrt(1.0 - r1);
       const double phi = 2.0 * kPiD * r2;
@@ -1134,11 +1138,16 @@ bool lean_path(const TraceParams& P) {
   return P.n_levels == 1 && P.n_temps >= 2 && P.lean &&
          P.lv[0].n[0] * static_cast<int64_t>(P.lv[0].n[1]) * P.lv[0].n[2] < (1LL << 31);
 }
-size_t fp64_smem(const TraceParams& P) { return lean_path(P) ? 3 * kBlock * sizeof(int4) : 0; }
+size_t fp64_smem(const TraceParams& P) {
+  return lean_path(P) ? kLeanRecs64 * kBlock * sizeof(int4) : 0;
+}
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (lean_path(P))
-    return min_blocks >= 6 ? trace_pool_fp64_lean<6>
-                           : (min_blocks >= 5 ? trace_pool_fp64_lean<5> : trace_pool_fp64_lean<4>);
+    return min_blocks >= 8   ? trace_pool_fp64_lean<8>
+           : min_blocks == 7 ? trace_pool_fp64_lean<7>
+           : min_blocks == 6 ? trace_pool_fp64_lean<6>
+           : min_blocks == 5 ? trace_pool_fp64_lean<5>
+                             : trace_pool_fp64_lean<4>;
   return nullptr;
 }
 TraceFn fp64_kernel(bool multi, int min_blocks) {
