@@ -181,6 +181,7 @@ struct Tune {
   int fp64_min_blocks = 6;
   int fp32_min_blocks = 6;
   int lean = 1;
+  int cache_hint = 0;
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -194,6 +195,7 @@ const Tune& tune() {
     x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
     x.lean = env_int("ERMC_LEAN", x.lean);
+    x.cache_hint = env_int("ERMC_CACHE_HINT", x.cache_hint);
     return x;
   }();
   return t;
@@ -522,6 +524,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.refill_threshold = tune().refill;
   P.inner_steps = tune().inner_steps;
   P.lean = tune().lean;
+  P.cache_hint = tune().cache_hint;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;

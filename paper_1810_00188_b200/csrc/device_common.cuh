@@ -45,6 +45,54 @@ __device__ __forceinline__ double4 ldg4(const double4* p) {
   return r;
 }
 
+// Cache-hinted read-only loads for the march (kHint: 0 = plain LDG.CONSTANT,
+// 1 = temperature gathers bypass L1 allocation, 2 = temperature gathers evict
+// first; for kHint >= 1 the interval records are kept with evict_last).
+template <int kHint>
+__device__ __forceinline__ float ld_t32(const float* p) {
+  float r;
+  if (kHint == 1)
+    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  else if (kHint == 2)
+    asm("ld.global.nc.L1::evict_first.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  else
+    r = __ldg(p);
+  return r;
+}
+template <int kHint>
+__device__ __forceinline__ double ld_t64(const double* p) {
+  double r;
+  if (kHint == 1)
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  else if (kHint == 2)
+    asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  else
+    r = __ldg(p);
+  return r;
+}
+template <int kHint>
+__device__ __forceinline__ float4 ld_rec32(const float4* p) {
+  if (kHint == 0) return __ldg(p);
+  float4 r;
+  asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+  return r;
+}
+template <int kHint>
+__device__ __forceinline__ double4 ld_rec64(const double4* p) {
+  double4 r;
+  if (kHint == 0)
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+        : "l"(p));
+  else
+    asm("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+        : "l"(p));
+  return r;
+}
+
 // std::upper_bound over a short ascending array (sampling.cpp:44-51).
 __device__ __forceinline__ int upper_bound_d(const double* a, int n, double x) {
   int first = 0, count = n;

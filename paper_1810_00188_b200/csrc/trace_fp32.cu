@@ -312,6 +312,7 @@ struct Fp32Tracer {
 //            a non-moving axis},
 // so one LDS.128 replaces the predicated per-axis selects and param-space
 // loads of a register-only DDA; `lin` carries the cell index.
+template <int kHint>
 struct Fp32Lean {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
@@ -398,7 +399,7 @@ struct Fp32Lean {
     const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
     const int lo = min(static_cast<int>(u), P.n_temps - 2);
     const float f = u - static_cast<float>(lo);
-    const float4 v = __ldg(row + lo);
+    const float4 v = ld_rec32<kHint>(row + lo);
 
     int axis = 0;
     float tmin = tn[0];
@@ -423,7 +424,7 @@ struct Fp32Lean {
     const bool inside = left >= 0;
     const int nlin = lin + r.y + (inside ? 0 : r.w);  // periodic image if outside
     float t_next = t_cur;
-    if (inside || P.periodic[axis]) t_next = __ldg(L.field32 + nlin);
+    if (inside || P.periodic[axis]) t_next = ld_t32<kHint>(L.field32 + nlin);
 
     const float kappa = fmaf(f, v.y, v.x);
     const float ib2n = fmaf(f, v.w, v.z);
@@ -509,10 +510,10 @@ struct Fp32Lean {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-template <int kMinBlocks>
+template <int kMinBlocks, int kHint>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_lean(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp32Lean, false>(P);
+  pool_kernel_body<Fp32Lean<kHint>, false>(P);
 }
 
 struct Fp32Multi : Fp32Tracer {
@@ -568,7 +569,7 @@ size_t fp32_smem(const TraceParams& P) {
 }
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   if (fp32_lean(P))
-    return min_blocks >= 8 ? trace_pool_fp32_lean<8> : trace_pool_fp32_lean<6>;
+    return min_blocks >= 8 ? trace_pool_fp32_lean<8, 0> : trace_pool_fp32_lean<6, 0>;
   return min_blocks >= 8 ? trace_pool_fp32<8> : trace_pool_fp32<6>;
 }
 }  // namespace

@@ -406,6 +406,7 @@ __device__ __noinline__ int exact_index(double T, double t0, double dt) {
 // SpectralModel::lookup on the packed tables (uniform or not). The interval
 // record of the returned lo is loaded into *rec (issued together with the
 // temperature record so the two loads overlap).
+template <int kHint = 0>
 __device__ __forceinline__ bool fast_lookup(const TraceParams& P,
                                             const double4* row, double T,
                                             int& lo, double& frac,
@@ -421,14 +422,14 @@ __device__ __forceinline__ bool fast_lookup(const TraceParams& P,
     else
       l = static_cast<int>(x);
     l = min(max(l, 0), nt - 2);
-    double4 ti = ldg4(P.tint + l);
-    rec = ldg4(row + l);
+    double4 ti = ld_rec64<kHint>(P.tint + l);
+    rec = ld_rec64<kHint>(row + l);
     double f = div_rcp(T - ti.x, ti.y, ti.z);
     if ((f < 0.0 && l > 0) || (f > 1.0 && l < nt - 2)) {
       // rounding put T in the neighbouring interval (spectral.cpp:159-168)
       l += f < 0.0 ? -1 : 1;
-      ti = ldg4(P.tint + l);
-      rec = ldg4(row + l);
+      ti = ld_rec64<kHint>(P.tint + l);
+      rec = ld_rec64<kHint>(row + l);
       f = div_rcp(T - ti.x, ti.y, ti.z);
     }
     lo = l;
@@ -688,6 +689,7 @@ __device__ __forceinline__ double expm1_lean(double x) {
 // rec[3] = {band, next_draw, cell id, ray id}: state only walls touch.
 constexpr int kLeanRecs64 = 4;
 
+template <int kHint>
 struct Fp64Lean {
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
@@ -760,7 +762,7 @@ struct Fp64Lean {
     int lo;
     double frac;
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
-    if (!fast_lookup(P, P.iv64 + row, t_cur, lo, frac, v)) {
+    if (!fast_lookup<kHint>(P, P.iv64 + row, t_cur, lo, frac, v)) {
       err = kErrTableRange;
       return kFail;
     }
@@ -785,7 +787,7 @@ struct Fp64Lean {
     int nlin = lin + rec.z;
     if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
     double t_next = t_cur;
-    if (inside || periodic) t_next = __ldg(L.field + nlin);
+    if (inside || periodic) t_next = ld_t64<kHint>(L.field + nlin);
 
     const double kappa = frac == 0.0 ? v.x : v.x + frac * (v.y - v.x);
     const double ib2 = frac == 0.0 ? v.z : v.z + frac * (v.w - v.z);
@@ -930,10 +932,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     pool_kernel_body<Fp64Fast, false>(P);
 }
 
-template <int kMinBlocks>
+template <int kMinBlocks, int kHint>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp64Lean, false>(P);
+  pool_kernel_body<Fp64Lean<kHint>, false>(P);
 }
 
 // Debug/test kernel: one thread traces one explicit ray with full
@@ -1142,13 +1144,10 @@ size_t fp64_smem(const TraceParams& P) {
   return lean_path(P) ? kLeanRecs64 * kBlock * sizeof(int4) : 0;
 }
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
-  if (lean_path(P))
-    return min_blocks >= 8   ? trace_pool_fp64_lean<8>
-           : min_blocks == 7 ? trace_pool_fp64_lean<7>
-           : min_blocks == 6 ? trace_pool_fp64_lean<6>
-           : min_blocks == 5 ? trace_pool_fp64_lean<5>
-                             : trace_pool_fp64_lean<4>;
-  return nullptr;
+  if (!lean_path(P)) return nullptr;
+  return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0>
+         : min_blocks == 6 ? trace_pool_fp64_lean<6, 0>
+                           : trace_pool_fp64_lean<5, 0>;
 }
 TraceFn fp64_kernel(bool multi, int min_blocks) {
   if (multi) return min_blocks >= 5 ? trace_pool_fp64<true, 5> : trace_pool_fp64<true, 4>;
