@@ -53,6 +53,8 @@ cudaError_t launch_build_iv32(const double* k, const double* ib, int nb,
                               int nq, int nt, float4* iv, cudaStream_t s);
 cudaError_t launch_to_fp32(const double* src, float* dst, int64_t n,
                            cudaStream_t s);
+cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny,
+                                   int nz, cudaStream_t s);
 }  // namespace ermc_dev
 
 using ermc::Error;
@@ -182,6 +184,7 @@ struct Tune {
   int fp32_min_blocks = 6;
   int lean = 1;
   int cache_hint = 0;
+  int brick = 1;
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -196,6 +199,7 @@ const Tune& tune() {
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
     x.lean = env_int("ERMC_LEAN", x.lean);
     x.cache_hint = env_int("ERMC_CACHE_HINT", x.cache_hint);
+    x.brick = env_int("ERMC_BRICK", x.brick);
     return x;
   }();
   return t;
@@ -223,6 +227,7 @@ struct ermc_session {
   std::vector<std::unique_ptr<DevBuf<double>>> d_levels;  // levels >= 1
   std::vector<ermc_grid_t> level_grids;
   DevBuf<float> d_field32;
+  DevBuf<float> d_field32b;
   std::vector<std::unique_ptr<DevBuf<float>>> d_levels32;
   DevBuf<float4> d_iv32;
   bool iv32_ready = false;
@@ -705,6 +710,7 @@ void set_field_impl(ermc_session* s, const double* t, int is_device,
   s->iv32_ready = s->iv32_ready;  // tables unchanged
   s->d_levels32.clear();
   s->d_field32.reset();
+  s->d_field32b.reset();
 }
 
 void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
@@ -732,6 +738,19 @@ void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
     ++s->launches;
   }
   P.lv[0].field32 = s->d_field32.p;
+  const ermc_grid_t& g0 = s->grid;
+  const bool even = g0.nx % 2 == 0 && g0.ny % 2 == 0 && g0.nz % 2 == 0;
+  P.brick = (tune().brick && even && s->config.n_levels == 1) ? 1 : 0;
+  if (P.brick) {
+    if (!s->d_field32b.p) {
+      s->d_field32b.ensure(static_cast<size_t>(s->n_cells));
+      cuda_check(ermc_dev::launch_to_fp32_bricked(s->d_field.p, s->d_field32b.p, g0.nx,
+                                                  g0.ny, g0.nz, st),
+                 "to_fp32_bricked");
+      ++s->launches;
+    }
+    P.lv[0].field32b = s->d_field32b.p;
+  }
   s->d_levels32.resize(s->config.n_levels);
   for (int l = 1; l < s->config.n_levels; ++l) {
     const int64_t n = cells_of(s->level_grids[l]);

@@ -93,6 +93,16 @@ __device__ __forceinline__ double4 ld_rec64(const double4* p) {
   return r;
 }
 
+// Element index of cell (i, j, k) in the 2x2x2 micro-brick layout: bricks in
+// k-fastest order, cells inside a brick as (i&1, j&1, k&1) -> 4i + 2j + k.
+// A brick of fp32 values is one 32-byte sector; a ray step stays inside its
+// brick with probability ~1/2, so consecutive gathers share L1 sectors.
+__device__ __forceinline__ int brick_index(const LevelDesc& L, int i, int j, int k) {
+  const int nby = (L.n[1] + 1) >> 1, nbz = (L.n[2] + 1) >> 1;
+  return (((i >> 1) * nby + (j >> 1)) * nbz + (k >> 1)) * 8 + ((i & 1) << 2) +
+         ((j & 1) << 1) + (k & 1);
+}
+
 // std::upper_bound over a short ascending array (sampling.cpp:44-51).
 __device__ __forceinline__ int upper_bound_d(const double* a, int n, double x) {
   int first = 0, count = n;

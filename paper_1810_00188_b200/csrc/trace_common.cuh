@@ -23,6 +23,7 @@ struct LevelDesc {
   double eps;        // geom_eps = 1e-12 * min spacing (geometry.hpp:114-116)
   const double* field;   // fp64 temperature, k-fastest
   const float* field32;  // fp32 copy for the fast kernel (may be null)
+  const float* field32b;   // fp32 in 2x2x2 micro-bricks (even grids, lean kernel)
 };
 
 // Error codes raised on the device; the host re-traces the failing ray
@@ -84,6 +85,7 @@ struct TraceParams {
   int32_t inner_steps;       // march steps between two pool checks
   int32_t lean;              // fp64: 1 = lean tracer (per-axis records in smem)
   int32_t cache_hint;        // L1 policy of the lean tracers' loads (0, 1, 2)
+  int32_t brick;             // fp32 lean tracer reads the micro-brick field copy
   int64_t cell_base;         // first global linear cell of this chunk
   int64_t n_cells;           // cells in this chunk
   uint64_t n_work;           // n_cells * rays (ray work items)

@@ -510,6 +510,245 @@ struct Fp32Lean {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
+// Micro-brick variant of the lean tracer (grids with even dimensions): the
+// fp32 field is stored in 2x2x2 bricks (one 32-byte sector each) and the
+// per-axis record carries the two signed index deltas of a step,
+//   rec[a] = {t_delta bits, cells left before the face, delta inside a brick,
+//             delta across a brick face}   (moving axis)
+//            {inf, INT_MAX, 0, fixed index}                 (non-moving axis).
+// With even n a step leaves its brick exactly when the cells-left counter is
+// even before the step, for either direction.
+struct Fp32Brick {
+  float p0[3], dir[3], tn[3];
+  float s, tau, acc, ib1n, last_ib2n, t_cur;
+  double cq;
+  const float4* row;
+  int4* ax;
+  int lin, band, steps_;
+  uint32_t next_draw, ray_id;
+  uint64_t h_cell;
+  int err;
+
+  __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
+    const int4 r = ax[a * kBlock32];
+    if (r.z == 0) return r.w;
+    return r.z > 0 ? L.n[a] - 1 - r.y : r.y;
+  }
+
+  __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx) {
+    const int nby = (L.n[1] + 1) >> 1, nbz = (L.n[2] + 1) >> 1;
+    const int bs[3] = {nby * nbz, nbz, 1};
+    const int sn[3] = {4, 2, 1};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float da = dir[a];
+      if (da == 0.0f) {
+        tn[a] = __int_as_float(0x7f800000);
+        ax[a * kBlock32] = make_int4(0x7f800000, 0x7fffffff, 0, idx[a]);
+        continue;
+      }
+      const float inv = 1.0f / da;
+      const bool up = da > 0.0f;
+      const float face =
+          static_cast<float>(L.origin[a] + (idx[a] + (up ? 1 : 0)) * L.d[a]);
+      tn[a] = (face - p0[a]) * inv;
+      const float td = static_cast<float>(L.d[a]) * fabsf(inv);
+      const int near = up ? sn[a] : -sn[a];
+      const int far = up ? 8 * bs[a] - sn[a] : sn[a] - 8 * bs[a];
+      ax[a * kBlock32] =
+          make_int4(__float_as_int(td), up ? L.n[a] - 1 - idx[a] : idx[a], near, far);
+    }
+    s = 0.0f;
+    lin = brick_index(L, idx[0], idx[1], idx[2]);
+  }
+
+  __device__ __forceinline__ void rebase() {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      p0[a] = fmaf(s, dir[a], p0[a]);
+      tn[a] -= s;
+    }
+    s = 0.0f;
+  }
+
+  __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
+                                      uint32_t ray) {
+    extern __shared__ int4 s_dyn[];
+    ax = s_dyn + threadIdx.x;
+    Fp32Tracer base;
+    const int e = base.init(P, cell, ray);
+    if (e != kErrNone) return e;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      p0[a] = base.p0[a];
+      dir[a] = base.dir[a];
+    }
+    tau = 1.0f;
+    acc = 0.0f;
+    ib1n = base.ib1n;
+    last_ib2n = base.ib1n;
+    cq = base.cq;
+    row = base.row;
+    band = base.band;
+    steps_ = 0;
+    next_draw = base.next_draw;
+    ray_id = ray;
+    h_cell = base.h_cell;
+    t_cur = base.t_cur;  // the same value as the brick copy's
+    setup(P.lv[0], base.idx);
+    return kErrNone;
+  }
+
+  __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
+    if (tau <= P.tol32) return kDone;
+    if (steps_ >= max_steps) return kDone;
+    const LevelDesc& L = P.lv[0];
+    const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
+    const int lo = min(static_cast<int>(u), P.n_temps - 2);
+    const float f = u - static_cast<float>(lo);
+    const float4 v = __ldg(row + lo);
+
+    int axis = 0;
+    float tmin = tn[0];
+    if (tn[1] < tmin) {
+      tmin = tn[1];
+      axis = 1;
+    }
+    if (tn[2] < tmin) {
+      tmin = tn[2];
+      axis = 2;
+    }
+    const float ds = fmaxf(tmin - s, 0.0f);
+    s = fmaxf(tmin, s);
+
+    int4* rp = ax + axis * kBlock32;
+    const int4 r = *rp;
+    const float td = __int_as_float(r.x);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (a == axis) tn[a] += td;
+    const int left = r.y - 1;
+    const bool inside = left >= 0;
+    const bool periodic = (P.periodic_mask >> axis) & 1;
+    int nlin = lin + ((r.y & 1) ? r.z : r.w);
+    float t_next = t_cur;
+    if (inside) {
+      t_next = __ldg(L.field32b + nlin);
+    } else if (periodic) {
+      int idx[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        idx[a] = a == axis ? (r.z > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
+      nlin = brick_index(L, idx[0], idx[1], idx[2]);
+      t_next = __ldg(L.field32b + nlin);
+    }
+
+    const float kappa = fmaf(f, v.y, v.x);
+    const float ib2n = fmaf(f, v.w, v.z);
+    const float alpha = absorb32(kappa * ds);
+    last_ib2n = ib2n;
+    const float ta = tau * alpha;
+    acc = fmaf(ta, ib2n - ib1n, acc);
+    tau -= ta;
+    ++steps_;
+
+    if (inside) {
+      rp->y = left;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    if (periodic) {
+      rp->y = L.n[axis] - 1;
+      rebase();
+      const float ext = static_cast<float>(L.extent[axis]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) p0[a] += r.z > 0 ? -ext : ext;
+      lin = nlin;
+      t_cur = t_next;
+      return kContinue;
+    }
+    // wall exchange (tracer.cpp:155-165); the ray stays in its cell
+    const bool at_hi = r.z > 0;
+    const int face = 2 * axis + (at_hi ? 1 : 0);
+    const float ew = static_cast<float>(P.wall_eps[face]);
+    const float ibw = __ldg(P.wall_ibn32 + face * P.n_bands + band);
+    const float tw = tau * ew;
+    acc = fmaf(tw, ibw - ib1n, acc);
+    tau -= tw;
+    if (tau <= P.tol32) return kDone;
+    // reflection (tracer.cpp:167-182)
+    int idx[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);  // left still 0: the boundary cell
+    rebase();
+    const float face_pos =
+        static_cast<float>(L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
+    float nd[3] = {dir[0], dir[1], dir[2]};
+    if (P.specular) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (a == axis) nd[a] = -nd[a];
+    } else {
+      const double r1 = draw_u(h_cell, ray_id, next_draw++);
+      const double r2 = draw_u(h_cell, ray_id, next_draw++);
+      const float sin_t = sqrtf(static_cast<float>(r1));
+      const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
+      float sp, cp;
+      sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
+      const int t1 = axis == 2 ? 0 : axis + 1;
+      const int t2 = axis == 0 ? 2 : axis - 1;
+      const float inward = at_hi ? -1.0f : 1.0f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a == axis) nd[a] = inward * cos_t;
+        if (a == t1) nd[a] = sin_t * cp;
+        if (a == t2) nd[a] = sin_t * sp;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a == axis) p0[a] = face_pos;
+      dir[a] = nd[a];
+    }
+    setup(L, idx);
+    return kContinue;
+  }
+
+  __device__ __forceinline__ double finish(const TraceParams&) const {
+    return cq * static_cast<double>(fmaf(tau, last_ib2n - ib1n, acc));
+  }
+  __device__ __forceinline__ bool finite_state() const {
+    return isfinite(tau) && isfinite(acc);
+  }
+  __device__ __forceinline__ int level() const { return 0; }
+  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int steps() const { return steps_; }
+};
+
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kBlock32, kMinBlocks)
+    trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
+  pool_kernel_body<Fp32Brick, false>(P);
+}
+
+// Converts the fp64 k-fastest field to the fp32 micro-brick layout.
+__global__ void to_fp32_bricked(const double* __restrict__ src, float* __restrict__ dst,
+                                int nx, int ny, int nz) {
+  const int64_t n = static_cast<int64_t>(nx) * ny * nz;
+  const int nby = (ny + 1) >> 1, nbz = (nz + 1) >> 1;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < n;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(c / (static_cast<int64_t>(ny) * nz));
+    const int j = static_cast<int>((c / nz) % ny);
+    const int k = static_cast<int>(c % nz);
+    const int64_t b = ((static_cast<int64_t>(i >> 1) * nby + (j >> 1)) * nbz + (k >> 1)) * 8 +
+                      ((i & 1) << 2) + ((j & 1) << 1) + (k & 1);
+    dst[b] = static_cast<float>(src[c]);
+  }
+}
+
 template <int kMinBlocks, int kHint>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_lean(const __grid_constant__ TraceParams P) {
@@ -568,6 +807,8 @@ size_t fp32_smem(const TraceParams& P) {
   return fp32_lean(P) ? 3 * kBlock32 * sizeof(int4) : 0;
 }
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
+  if (fp32_lean(P) && P.brick)
+    return min_blocks >= 8 ? trace_pool_fp32_brick<8> : trace_pool_fp32_brick<6>;
   if (fp32_lean(P))
     return min_blocks >= 8 ? trace_pool_fp32_lean<8, 0> : trace_pool_fp32_lean<6, 0>;
   return min_blocks >= 8 ? trace_pool_fp32<8> : trace_pool_fp32<6>;
@@ -593,6 +834,12 @@ cudaError_t launch_build_iv32(const double* k, const double* ib, int nb, int nq,
   if (n <= 0) return cudaSuccess;
   build_iv32<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
       k, ib, nb, nq, nt, iv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny,
+                                   int nz, cudaStream_t stream) {
+  to_fp32_bricked<<<1184, 256, 0, stream>>>(src, dst, nx, ny, nz);
   return cudaGetLastError();
 }
 

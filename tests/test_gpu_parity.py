@@ -159,3 +159,24 @@ def test_device_rng_is_the_reference_stream():
         want = np.array([refshim.uniform(seed, int(c), int(r), int(d))
                          for c, r, d in zip(cells, rays, draws)])
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name,n,variant", [
+    ("epsw-low", 10, {}),                       # even grid: micro-brick tracer, grey walls
+    ("epsw-low", 9, {}),                        # odd grid: linear-layout lean tracer
+    ("nb-3dimens", 10, dict(specular_walls=1)),  # all walls, specular
+    ("box-sin-5", 9, {}),
+    ("nb-parab", 12, dict(volume_sampling=1)),
+])
+def test_fp32_tracks_fp64_on_the_same_rays(name, n, variant):
+    # Same seed: the fp32 kernel traces the reference's rays (same draws,
+    # same (band, g)); per-cell results agree far inside the MC noise and the
+    # step counts agree to 1e-3 (fp32 DDA ties resolve differently rarely).
+    grid, t, b, m, _ = refshim.ref_case(name, n)
+    q64, sd64, _, t64, _ = capi.solve(grid, t, b, m, capi.config_struct(
+        rays_per_cell=32, seed=77, **variant))
+    q32, sd32, _, t32, _ = capi.solve(grid, t, b, m, capi.config_struct(
+        rays_per_cell=32, seed=77, precision=capi.FP32, **variant))
+    assert abs(t32 - t64) <= 1e-3 * t64, (t32, t64)
+    bad = three_sigma_violations(q64, q32, 0.1 * sd64, 0.1 * sd32)
+    assert bad <= allowed_3sigma(len(q64)), bad
