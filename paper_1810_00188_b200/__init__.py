@@ -8,7 +8,7 @@ table builders, KTAB1/TFLD1/QRF1 I/O and `solve` — which runs every cell and
 ray on the GPU through the C-ABI in include/ermc_b200.h.
 
 The compiled extension is required: importing without it raises ImportError
-(there is no CPU fallback). Run `python -m paper_1810_00188_b200.build` or
+(there is no CPU fallback). Run `python paper_1810_00188_b200/build.py` or
 `__graft_entry__.build()` first.
 """
 from __future__ import annotations
@@ -24,7 +24,7 @@ try:
 except ModuleNotFoundError as exc:  # pragma: no cover - only when unbuilt
     raise ImportError(
         "paper_1810_00188_b200: the compiled extension (_ermc / libermc_b200.so) "
-        "is missing; build it with `python -m paper_1810_00188_b200.build`. "
+        "is missing; build it with `python paper_1810_00188_b200/build.py`. "
         "There is no CPU fallback."
     ) from exc
 

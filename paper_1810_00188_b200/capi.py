@@ -114,7 +114,7 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
     if _lib is not None and path == LIB_PATH:
         return _lib
     if not Path(path).exists():
-        raise ImportError(f"{path} is missing: build with `python -m paper_1810_00188_b200.build`"
+        raise ImportError(f"{path} is missing: build with `python paper_1810_00188_b200/build.py`"
                           " (there is no CPU fallback)")
     lib = C.CDLL(str(path))
     for name, (res, args) in EXPORTS.items():
