@@ -12,6 +12,7 @@
 #pragma once
 
 #include <array>
+#include <cstddef>
 #include <cstdint>
 #include <iosfwd>
 #include <limits>
@@ -262,6 +263,16 @@ StepCensus step_census(const SolutionField& solution, const CartesianGrid& grid,
                        const TemperatureField& field,
                        const BoundarySpec& boundary,
                        const SpectralModel& model, const SolveConfig& config);
+
+// ---- oracles.hpp (the line-by-line path only) -------------------------------
+// lbl_model / lbl_reference (reference oracles.hpp:50-59): one band per
+// spectral sample, one g point; lbl_reference solves it on the GPU.
+SpectralModel lbl_model(const LineSpectrum& spectrum,
+                        std::size_t memory_cap_bytes = std::size_t(2) << 30);
+SolutionField lbl_reference(const CartesianGrid& grid, const TemperatureField& field,
+                            const BoundarySpec& boundary, const LineSpectrum& spectrum,
+                            const SolveConfig& config,
+                            std::size_t memory_cap_bytes = std::size_t(2) << 30);
 
 // ---- io.hpp ----------------------------------------------------------------
 void write_ktab(const std::string& path, const SpectralModel& model);

@@ -548,6 +548,50 @@ SolutionField solve(const CartesianGrid& grid, const TemperatureField& field,
   return out;
 }
 
+// Line-by-line model (reference oracles.cpp:232-264): every spectral sample
+// becomes its own band — edges at the midpoints between samples, the outer
+// edges mirrored half a spacing out — with a single g point, so the solve
+// samples wavenumbers directly. The GPU solve then runs unchanged with
+// n_bands = number of samples (8001 for the default Elsasser spectrum).
+SpectralModel lbl_model(const LineSpectrum& spectrum, std::size_t memory_cap_bytes) {
+  spectrum.validate();
+  const std::vector<double>& nu = spectrum.nu_grid;
+  const size_t ns = nu.size();
+  const size_t nt = spectrum.temps.size();
+  const size_t need = ns * nt * 2 * sizeof(double);
+  if (need > memory_cap_bytes)
+    throw Error("lbl_model: tables would need " + std::to_string(need) +
+                " bytes; coarsen the spectrum or raise the cap");
+  std::vector<NarrowBand> bands(ns);
+  for (size_t s = 0; s < ns; ++s) {
+    NarrowBand& b = bands[s];
+    b.nu_center = nu[s];
+    b.nu_lo = s > 0 ? 0.5 * (nu[s - 1] + nu[s]) : nu[0] - 0.5 * (nu[1] - nu[0]);
+    b.nu_hi = s + 1 < ns ? 0.5 * (nu[s] + nu[s + 1])
+                         : nu[ns - 1] + 0.5 * (nu[ns - 1] - nu[ns - 2]);
+  }
+  std::vector<double> k_table(ns * nt), ib_table(ns * nt);
+  for (size_t s = 0; s < ns; ++s) {
+    double* krow = k_table.data() + s * nt;
+    double* irow = ib_table.data() + s * nt;
+    for (size_t t = 0; t < nt; ++t) {
+      krow[t] = spectrum.kappa[t][s];
+      irow[t] = band_blackbody(bands[s], spectrum.temps[t]);
+    }
+  }
+  return SpectralModel(std::move(bands), QuadratureSet::single_point(), spectrum.temps,
+                       std::move(k_table), std::move(ib_table));
+}
+
+// lbl_reference (reference oracles.cpp:266-274): the line-by-line solve, on
+// the GPU like every other solve.
+SolutionField lbl_reference(const CartesianGrid& grid, const TemperatureField& field,
+                            const BoundarySpec& boundary, const LineSpectrum& spectrum,
+                            const SolveConfig& config, std::size_t memory_cap_bytes) {
+  const SpectralModel model = lbl_model(spectrum, memory_cap_bytes);
+  return solve(grid, field, boundary, model, config);
+}
+
 StepCensus step_census(const SolutionField& solution, const CartesianGrid& grid,
                        const TemperatureField& field,
                        const BoundarySpec& boundary,

@@ -180,3 +180,43 @@ def test_fp32_tracks_fp64_on_the_same_rays(name, n, variant):
     assert abs(t32 - t64) <= 1e-3 * t64, (t32, t64)
     bad = three_sigma_violations(q64, q32, 0.1 * sd64, 0.1 * sd32)
     assert bad <= allowed_3sigma(len(q64)), bad
+
+
+def _lbl_inputs(mod, n, t_fn, wall):
+    g = mod.CartesianGrid()
+    g.nx = g.ny = g.nz = n
+    g.dx = g.dy = g.dz = 1.0 / n
+    f = mod.TemperatureField()
+    f.grid = g
+    f.values = [t_fn((i + 0.5) / n) for i in range(n) for _ in range(n * n)]
+    b = mod.BoundarySpec()
+    b.lo = [mod.Wall(wall, 1.0)] * 3
+    b.hi = [mod.Wall(wall, 1.0)] * 3
+    return g, f, b
+
+
+@pytest.mark.parametrize("profile", ["isothermal", "parab"])
+def test_lbl_reference_matches_reference(profile):
+    # lbl_reference (oracles.cpp:266-274) through the drop-in Python module:
+    # the default Elsasser spectrum (8001 line-by-line bands, one g point)
+    # on the test_oracles.cpp:117-163 temperature nodes.
+    import paper_1810_00188_b200 as E
+    R = refshim.ref_module()
+    temps = [500.0, 1000.0, 1500.0]
+    t_fn = (lambda x: 1000.0) if profile == "isothermal" else \
+        (lambda x: 600.0 + 1600.0 * x * (1.0 - x))
+    out = []
+    for mod in (E, R):
+        sp = mod.elsasser_spectrum(temps)
+        assert len(sp.nu_grid) == 8001
+        g, f, b = _lbl_inputs(mod, 6, t_fn, 1000.0 if profile == "isothermal" else 600.0)
+        cfg = mod.SolveConfig()
+        cfg.rays_per_cell = 40
+        cfg.seed = 5
+        out.append(mod.lbl_reference(g, f, b, sp, cfg))
+    s, r = out
+    if profile == "isothermal":
+        assert all(q == 0.0 for q in s.q_r)
+    assert s.total_steps == r.total_steps
+    assert_fp64_parity(np.asarray(s.q_r), np.asarray(r.q_r),
+                       np.asarray(s.std_dev), np.asarray(r.std_dev))

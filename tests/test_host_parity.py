@@ -178,3 +178,52 @@ def test_solve_without_gpu_fails_loudly():
 def test_channel_field_matches_survey_range():
     t = W.channel_field(64)
     assert 575.0 < t.min() < 577.0 and 951.0 < t.max() < 953.0  # [576, 952]
+
+
+@needs_ref
+def test_lbl_model_matches_reference_tables():
+    # lbl_model (reference oracles.cpp:232-264), restated on the reference's
+    # own spectrum and planck_intensity: one band per sample, midpoint edges,
+    # kappa transposed to [sample][T], Ib(nu_s, T) (0 at T <= 0).
+    R = refshim.ref_module()
+    for temps in ([500.0, 1000.0, 1500.0], [450.0 + 50.0 * j for j in range(13)]):
+        sp = R.elsasser_spectrum(temps)
+        nu = np.asarray(sp.nu_grid)
+        kap = np.asarray(sp.kappa)
+        m = E.lbl_model(E.elsasser_spectrum(temps))
+        assert m.n_bands() == len(nu) and m.n_quad() == 1
+        assert np.array_equal(np.asarray(m.k_table()), kap.T.reshape(-1))
+        ib = np.array([[R.planck_intensity(v, t) if t > 0 else 0.0 for t in temps]
+                       for v in nu])
+        assert np.array_equal(np.asarray(m.ib_table()), ib.reshape(-1))
+        lo = np.array([b.nu_lo for b in m.bands()])
+        hi = np.array([b.nu_hi for b in m.bands()])
+        assert lo[0] == nu[0] - 0.5 * (nu[1] - nu[0])
+        assert hi[-1] == nu[-1] + 0.5 * (nu[-1] - nu[-2])
+        assert np.array_equal(lo[1:], 0.5 * (nu[:-1] + nu[1:]))
+        assert np.array_equal(hi[:-1], 0.5 * (nu[:-1] + nu[1:]))
+
+
+def test_lbl_flat_spectrum_is_the_grey_model_bitwise():
+    # test_oracles.cpp:124-137
+    temps = [500.0, 1000.0, 1500.0]
+    grey = E.LineSpectrum()
+    grey.temps = temps
+    grey.nu_grid = [400.0 + 2.5 * i for i in range(201)]
+    grey.kappa = [[2.0] * 201 for _ in temps]
+    lbl = E.lbl_model(grey)
+    direct = E.grey_model(2.0, lbl.bands(), temps, E.QuadratureSet.single_point())
+    assert lbl.k_table() == direct.k_table()
+    assert lbl.ib_table() == direct.ib_table()
+    assert lbl.n_bands() == 201 and lbl.n_quad() == 1
+
+
+def test_lbl_memory_cap_is_enforced():
+    # test_oracles.cpp:158-162: the cap is checked before any table is built.
+    sp = E.elsasser_spectrum([500.0, 1000.0, 1500.0])
+    with pytest.raises(RuntimeError, match="bytes"):
+        E.lbl_model(sp, 1024)
+    grid = E.CartesianGrid()
+    field = E.TemperatureField()
+    with pytest.raises(RuntimeError, match="lbl_model: tables would need"):
+        E.lbl_reference(grid, field, E.BoundarySpec(), sp, E.SolveConfig(), 1024)
