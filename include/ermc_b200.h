@@ -156,8 +156,9 @@ int ermc_b200_session_solve(ermc_session_t* s, int64_t cell_lo,
                             char* errbuf, size_t errlen);
 
 /* Per-kernel device times (CUDA events on the launch stream) of the last
- * session_solve, milliseconds: [0] validate+T_max, [1] restrict,
- * [2] trace (all chunks), [3] per-cell reduce. Also the launch count. */
+ * session_solve, milliseconds: [0] validate+T_max, [1] restrict + the
+ * narrow-band sort of the dispatch order, [2] trace (all chunks),
+ * [3] per-cell reduce. Also the launch count. */
 int ermc_b200_session_timings(const ermc_session_t* s, double* ms4,
                               int32_t* n_launches);
 
@@ -215,6 +216,12 @@ int ermc_b200_uniform_device(uint64_t seed, int64_t n, const uint64_t* cell_ids,
 int ermc_b200_device_count(void);
 /* ABI version for loaders. */
 int ermc_b200_abi_version(void);
+/* The solve entry points keep freed device buffers in a per-device cache
+ * (up to a third of the device memory) so repeated one-shot solves do not
+ * pay cudaMalloc/cudaFree; this returns the cached blocks of `device`
+ * (-1 = current) to the driver. No reference counterpart (the reference
+ * has no device memory). Returns 0. */
+int ermc_b200_release_cached_memory(int device);
 
 #ifdef __cplusplus
 }

@@ -35,6 +35,7 @@ CXX = shutil.which("g++") or "g++"
 CUDA_SOURCES = [
     ("trace_fp64.cu", ["--fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"]),
     ("trace_fp32.cu", []),
+    ("dispatch.cu", []),
     ("capi.cu", []),
 ]
 HOST_SOURCES = ["host_tables.cpp", "host_api.cpp", "host_io.cpp"]

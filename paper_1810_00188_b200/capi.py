@@ -98,6 +98,7 @@ EXPORTS = {
                                            _d, C.c_char_p, C.c_size_t]),
     "ermc_b200_device_count": (C.c_int, []),
     "ermc_b200_abi_version": (C.c_int, []),
+    "ermc_b200_release_cached_memory": (C.c_int, [C.c_int]),
 }
 
 

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <numeric>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -18,6 +19,8 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -55,6 +58,9 @@ cudaError_t launch_to_fp32(const double* src, float* dst, int64_t n,
                            cudaStream_t s);
 cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny,
                                    int nz, cudaStream_t s);
+int sort_max_bins();
+cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_bins,
+                           int tile_cells, uint16_t* keys, uint32_t* perm, cudaStream_t s);
 }  // namespace ermc_dev
 
 using ermc::Error;
@@ -95,6 +101,92 @@ struct DeviceGuard {
   }
 };
 
+// Process-wide caching allocator for device buffers. A one-shot solve
+// (ermc_b200_solve*) builds and drops a whole session — the field, the
+// per-ray scratch (8.6 GB at 256^3, R = 64), the dispatch order — so
+// without a cache every call pays cudaMalloc/cudaFree of all of it. Freed
+// blocks are kept per device (best fit within 2x of the request) up to a cap
+// of a third of the device memory; ermc_b200_release_cached_memory() returns
+// them. Every solve path synchronises its stream before its buffers are
+// released (session_solve_impl, solve_host, ~ermc_session), so a cached
+// block is never handed out while a kernel may still touch it.
+class DevicePool {
+ public:
+  static DevicePool& get() {
+    static DevicePool* pool = new DevicePool();  // never destroyed: no CUDA calls at exit
+    return *pool;
+  }
+  void* alloc(size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      auto& fl = free_[dev];
+      auto it = fl.lower_bound(bytes);
+      if (it != fl.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+        void* p = it->second;
+        cached_[dev] -= it->first;
+        size_[p] = it->first;
+        fl.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      release(dev);
+      cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    size_[p] = bytes;
+    return p;
+  }
+  void free(void* p) {
+    if (!p) return;
+    int dev = 0;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess) dev = a.device;
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = size_.find(p);
+    const size_t bytes = it == size_.end() ? 0 : it->second;
+    if (it != size_.end()) size_.erase(it);
+    free_[dev].emplace(bytes, p);
+    cached_[dev] += bytes;
+    trim_locked(dev);
+  }
+  void release(int dev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    DeviceGuard g(dev);
+    for (auto& kv : free_[dev]) cudaFree(kv.second);
+    free_[dev].clear();
+    cached_[dev] = 0;
+  }
+
+ private:
+  void trim_locked(int dev) {
+    if (cap_.find(dev) == cap_.end()) {
+      size_t fr = 0, tot = 0;
+      DeviceGuard g(dev);
+      cudaMemGetInfo(&fr, &tot);
+      cap_[dev] = tot / 3;
+    }
+    auto& fl = free_[dev];
+    while (cached_[dev] > cap_[dev] && !fl.empty()) {
+      auto last = std::prev(fl.end());
+      DeviceGuard g(dev);
+      cudaFree(last->second);
+      cached_[dev] -= last->first;
+      fl.erase(last);
+    }
+  }
+  std::mutex mu_;
+  std::map<int, std::multimap<size_t, void*>> free_;
+  std::map<int, size_t> cached_, cap_;
+  std::unordered_map<void*, size_t> size_;
+};
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -104,15 +196,14 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) DevicePool::get().free(p);
     p = nullptr;
     n = 0;
   }
   void ensure(size_t count) {
     if (count <= n && p) return;
     reset();
-    cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)),
-               "cudaMalloc");
+    p = static_cast<T*>(DevicePool::get().alloc(std::max<size_t>(count, 1) * sizeof(T)));
     n = count;
   }
   void upload(const T* src, size_t count, cudaStream_t s) {
@@ -185,6 +276,8 @@ struct Tune {
   int lean = 1;
   int cache_hint = 0;
   int brick = 1;
+  int sort = 1;  // narrow-band sorted dispatch (dispatch.cu)
+  int sort_tile_items = 1 << 16;
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -200,6 +293,8 @@ const Tune& tune() {
     x.lean = env_int("ERMC_LEAN", x.lean);
     x.cache_hint = env_int("ERMC_CACHE_HINT", x.cache_hint);
     x.brick = env_int("ERMC_BRICK", x.brick);
+    x.sort = env_int("ERMC_SORT", x.sort);
+    x.sort_tile_items = std::max(1, env_int("ERMC_SORT_TILE", x.sort_tile_items));
     return x;
   }();
   return t;
@@ -232,6 +327,10 @@ struct ermc_session {
   DevBuf<float4> d_iv32;
   bool iv32_ready = false;
   DevBuf<double> d_qray;
+  // narrow-band sorted dispatch: row rank by k(n,g,T_max), keys, order
+  DevBuf<int32_t> d_row_rank;
+  DevBuf<uint16_t> d_keys;
+  DevBuf<uint32_t> d_perm;
   DevBuf<unsigned long long> d_counters;  // per chunk: work, err key
   DevBuf<int32_t> d_errcode;
   DevBuf<unsigned long long> d_steps;
@@ -243,6 +342,16 @@ struct ermc_session {
   int32_t launches = 0;
   std::mutex mu;
   size_t qray_budget_bytes = 0;
+  // Marks the last asynchronous work (set_field's copy) so the destructor can
+  // wait for it before the buffers return to the pool.
+  cudaEvent_t last_work = nullptr;
+  ~ermc_session() {
+    if (last_work) {
+      DeviceGuard g(device);
+      cudaEventSynchronize(last_work);
+      cudaEventDestroy(last_work);
+    }
+  }
 };
 
 namespace {
@@ -289,9 +398,8 @@ ermc_session* create_session(const ermc_grid_t* grid,
   if (dev >= n_dev) throw Error("ermc_b200: device ordinal out of range");
   s->device = dev;
   DeviceGuard guard(dev);
-  cudaDeviceProp prop{};
-  cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
-  s->n_sm = prop.multiProcessorCount;
+  cuda_check(cudaDeviceGetAttribute(&s->n_sm, cudaDevAttrMultiProcessorCount, dev),
+             "cudaDeviceGetAttribute");
   s->grid = *grid;
   s->boundary = *boundary;
   s->config = *config;
@@ -358,6 +466,7 @@ struct Prepared {
   double qe = 0.0;
   std::vector<double> band_cdf, quad_cdf, kmax, ibmax, wall_ib;
   std::vector<float> wall_ibn32;
+  bool sorted = false;  // narrow-band sorted dispatch enabled for this solve
 };
 
 // Device stats pass + the reference's validation order (solver.cpp:39-58)
@@ -422,6 +531,18 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
     pr.ibmax[n] = ermc_host::interp_ib(v, n, t_max);
     for (int g = 0; g < v.nq; ++g)
       pr.kmax[static_cast<size_t>(n) * v.nq + g] = ermc_host::interp_k(v, n, g, t_max);
+  }
+  // Dispatch order of the spectral rows: k(n, g, T_max) ascending, ties in
+  // (n, g) order — the reference's presample_and_sort key (solver.cpp:62-80).
+  const int n_rows = v.nb * v.nq;
+  pr.sorted = tune().sort && n_rows <= ermc_dev::sort_max_bins();
+  if (pr.sorted) {
+    std::vector<int32_t> order(n_rows), rank(n_rows);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return pr.kmax[a] < pr.kmax[b]; });
+    for (int i = 0; i < n_rows; ++i) rank[order[i]] = i;
+    s->d_row_rank.upload(rank.data(), rank.size(), st);
   }
   pr.wall_ib.assign(6 * static_cast<size_t>(v.nb), 0.0);
   const ermc_boundary_t& b = s->boundary;
@@ -610,12 +731,20 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
   const int R = s->config.rays_per_cell;
   const int64_t total_cells = hi - lo;
   // Chunk so the per-ray buffer stays within budget and work ids fit 31 bits.
+  const size_t item_bytes = sizeof(double) + (pr.sorted ? sizeof(uint32_t) + sizeof(uint16_t) : 0);
   const uint64_t max_items = std::min<uint64_t>(
-      (1ull << 31) - 1, std::max<uint64_t>(s->qray_budget_bytes / sizeof(double), R));
+      (1ull << 31) - 1, std::max<uint64_t>(s->qray_budget_bytes / item_bytes, R));
   int64_t chunk_cells = std::max<int64_t>(1, static_cast<int64_t>(max_items / R));
   chunk_cells = std::min<int64_t>(chunk_cells, std::max<int64_t>(total_cells, 1));
   const int64_t n_chunks = total_cells == 0 ? 0 : (total_cells + chunk_cells - 1) / chunk_cells;
   s->d_qray.ensure(static_cast<size_t>(chunk_cells) * R);
+  const int n_rows = s->view.nb * s->view.nq;
+  if (pr.sorted) {
+    s->d_keys.ensure(static_cast<size_t>(chunk_cells) * R);
+    s->d_perm.ensure(static_cast<size_t>(chunk_cells) * R);
+  }
+  // ~2^16 work ids per sort tile (whole cells)
+  const int tile_cells = std::max(1, tune().sort_tile_items / R);
   s->d_counters.ensure(2 * std::max<int64_t>(n_chunks, 1));
   s->d_errcode.ensure(std::max<int64_t>(n_chunks, 1));
   cuda_check(cudaMemsetAsync(s->d_counters.p, 0,
@@ -630,7 +759,7 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
                        : ermc_dev::trace_fp64_blocks_per_sm(P, min_blocks);
   const int grid = std::max(1, bps) * s->n_sm;
 
-  std::vector<Timing> tt(n_chunks), tr(n_chunks);
+  std::vector<Timing> tt(n_chunks), tr(n_chunks), ts(n_chunks);
   for (int64_t ch = 0; ch < n_chunks; ++ch) {
     const int64_t c0 = lo + ch * chunk_cells;
     const int64_t nc = std::min<int64_t>(chunk_cells, hi - c0);
@@ -641,6 +770,18 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
     P.err_key = s->d_counters.p + 2 * ch + 1;
     P.err_code = s->d_errcode.p + ch;
     P.q_ray = s->d_qray.p;
+    P.perm = nullptr;
+    if (pr.sorted) {
+      cudaEventCreate(&ts[ch].a);
+      cudaEventCreate(&ts[ch].b);
+      cudaEventRecord(ts[ch].a, st);
+      cuda_check(ermc_dev::launch_ng_sort(P, s->d_row_rank.p, n_rows, tile_cells, s->d_keys.p,
+                                          s->d_perm.p, st),
+                 "narrow-band sort");
+      cudaEventRecord(ts[ch].b, st);
+      s->launches += 1;
+      P.perm = s->d_perm.p;
+    }
     cudaEventCreate(&tt[ch].a);
     cudaEventCreate(&tt[ch].b);
     cudaEventCreate(&tr[ch].a);
@@ -676,6 +817,13 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
     cudaEventElapsedTime(&b, tr[ch].a, tr[ch].b);
     s->ms[2] += a;
     s->ms[3] += b;
+    if (ts[ch].a) {
+      float c = 0.f;
+      cudaEventElapsedTime(&c, ts[ch].a, ts[ch].b);
+      s->ms[1] += c;
+      cudaEventDestroy(ts[ch].a);
+      cudaEventDestroy(ts[ch].b);
+    }
     cudaEventDestroy(tt[ch].a);
     cudaEventDestroy(tt[ch].b);
     cudaEventDestroy(tr[ch].a);
@@ -705,6 +853,9 @@ void set_field_impl(ermc_session* s, const double* t, int is_device,
                                        : cudaMemcpyHostToDevice,
                              st),
              "set_field copy");
+  if (!s->last_work)
+    cuda_check(cudaEventCreateWithFlags(&s->last_work, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(s->last_work, st), "event record");
   s->field_set = true;
   s->levels_valid = false;
   s->iv32_ready = s->iv32_ready;  // tables unchanged
@@ -1017,5 +1168,15 @@ int ermc_b200_device_count(void) {
 }
 
 int ermc_b200_abi_version(void) { return ERMC_B200_ABI_VERSION; }
+
+int ermc_b200_release_cached_memory(int device) {
+  int dev = device;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  DevicePool::get().release(dev);
+  return 0;
+}
 
 }  // extern "C"

@@ -155,7 +155,8 @@ __device__ __forceinline__ void raise_error(const TraceParams& P, uint64_t key,
 
 // Persistent ray pool. Every lane owns one ray; when at least
 // refill_threshold lanes of a warp are idle they take the next work items
-// (cell-major (cell, ray) ids) from a warp-local pool, refilled with one
+// (positions in the dispatch order: P.perm, or cell-major (cell, ray) ids)
+// from a warp-local pool, refilled with one
 // atomic per `kBatch` items from the chunk's global queue. Terminated rays
 // write their q to q_ray[ray][cell]; the per-cell reduction runs later in
 // ray-id order, so the schedule never changes a bit of the result.
@@ -211,6 +212,7 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         else if (rank - avail < nb_end - nb)
           w = nb + (rank - avail);
         if (w != 0xffffffffu) {
+          if (P.perm) w = __ldg(P.perm + w);  // narrow-band sorted order
           const uint32_t cell = w / rays;
           my_work = w;
           const int e = tr.init(P, P.cell_base + cell, w - cell * rays);

@@ -89,6 +89,8 @@ struct TraceParams {
   int64_t cell_base;         // first global linear cell of this chunk
   int64_t n_cells;           // cells in this chunk
   uint64_t n_work;           // n_cells * rays (ray work items)
+  const uint32_t* perm;      // dispatch order of the work ids (narrow-band
+                             // sorted, dispatch.cu) or null = cell-major
   unsigned long long* work_counter;
   double* q_ray;             // [rays][n_cells] per-ray q contributions
   unsigned long long* steps_per_level;  // [n_levels]
