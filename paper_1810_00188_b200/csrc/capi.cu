@@ -58,9 +58,12 @@ cudaError_t launch_to_fp32(const double* src, float* dst, int64_t n,
                            cudaStream_t s);
 cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny,
                                    int nz, cudaStream_t s);
+cudaError_t launch_to_bricked64(const double* src, double* dst, int nx, int ny, int nz,
+                                cudaStream_t s);
 int sort_max_bins();
+int sort_max_tile_items();
 cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_bins,
-                           int tile_cells, uint16_t* keys, uint32_t* perm, cudaStream_t s);
+                           int tile_cells, uint32_t* packed, uint32_t* perm, cudaStream_t s);
 }  // namespace ermc_dev
 
 using ermc::Error;
@@ -323,13 +326,14 @@ struct ermc_session {
   std::vector<ermc_grid_t> level_grids;
   DevBuf<float> d_field32;
   DevBuf<float> d_field32b;
+  DevBuf<double> d_field64b;
   std::vector<std::unique_ptr<DevBuf<float>>> d_levels32;
   DevBuf<float4> d_iv32;
   bool iv32_ready = false;
   DevBuf<double> d_qray;
   // narrow-band sorted dispatch: row rank by k(n,g,T_max), keys, order
   DevBuf<int32_t> d_row_rank;
-  DevBuf<uint16_t> d_keys;
+  DevBuf<uint32_t> d_keys;  // per work id: row rank << 16 | rank in its bin
   DevBuf<uint32_t> d_perm;
   DevBuf<unsigned long long> d_counters;  // per chunk: work, err key
   DevBuf<int32_t> d_errcode;
@@ -535,7 +539,8 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   // Dispatch order of the spectral rows: k(n, g, T_max) ascending, ties in
   // (n, g) order — the reference's presample_and_sort key (solver.cpp:62-80).
   const int n_rows = v.nb * v.nq;
-  pr.sorted = tune().sort && n_rows <= ermc_dev::sort_max_bins();
+  pr.sorted = tune().sort && n_rows <= ermc_dev::sort_max_bins() &&
+              c.rays_per_cell <= ermc_dev::sort_max_tile_items();
   if (pr.sorted) {
     std::vector<int32_t> order(n_rows), rank(n_rows);
     std::iota(order.begin(), order.end(), 0);
@@ -709,6 +714,23 @@ std::string describe_failure(ermc_session* s, const ermc_dev::TraceParams& P,
 void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
                         cudaStream_t st);
 
+// fp64 lean tracer: the micro-brick copy of the field (even grids, one level).
+void ensure_fp64_brick(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t st) {
+  const ermc_grid_t& g0 = s->grid;
+  const bool even = g0.nx % 2 == 0 && g0.ny % 2 == 0 && g0.nz % 2 == 0;
+  P.brick = (tune().brick && even && s->config.n_levels == 1 &&
+             s->n_cells < (int64_t(1) << 31)) ? 1 : 0;
+  if (!P.brick) return;
+  if (!s->d_field64b.p) {
+    s->d_field64b.ensure(static_cast<size_t>(s->n_cells));
+    cuda_check(ermc_dev::launch_to_bricked64(s->d_field.p, s->d_field64b.p, g0.nx, g0.ny,
+                                             g0.nz, st),
+               "to_bricked64");
+    ++s->launches;
+  }
+  P.lv[0].field64b = s->d_field64b.p;
+}
+
 // Core solve of [lo, hi) into device outputs.
 void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
                         double* d_sd, int64_t* steps_out, cudaStream_t st) {
@@ -726,12 +748,15 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
   prepare(s, pr, t_max, qe, /*build_levels=*/true, st);
   ermc_dev::TraceParams& P = pr.P;
   const bool fp32 = s->config.precision == ERMC_PRECISION_FP32;
-  if (fp32) ensure_fp32_inputs(s, P, st);
+  if (fp32)
+    ensure_fp32_inputs(s, P, st);
+  else
+    ensure_fp64_brick(s, P, st);
 
   const int R = s->config.rays_per_cell;
   const int64_t total_cells = hi - lo;
   // Chunk so the per-ray buffer stays within budget and work ids fit 31 bits.
-  const size_t item_bytes = sizeof(double) + (pr.sorted ? sizeof(uint32_t) + sizeof(uint16_t) : 0);
+  const size_t item_bytes = sizeof(double) + (pr.sorted ? 2 * sizeof(uint32_t) : 0);
   const uint64_t max_items = std::min<uint64_t>(
       (1ull << 31) - 1, std::max<uint64_t>(s->qray_budget_bytes / item_bytes, R));
   int64_t chunk_cells = std::max<int64_t>(1, static_cast<int64_t>(max_items / R));
@@ -743,8 +768,9 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
     s->d_keys.ensure(static_cast<size_t>(chunk_cells) * R);
     s->d_perm.ensure(static_cast<size_t>(chunk_cells) * R);
   }
-  // ~2^16 work ids per sort tile (whole cells)
-  const int tile_cells = std::max(1, tune().sort_tile_items / R);
+  // <= 2^16 work ids per sort tile (whole cells)
+  const int tile_cells = std::max(
+      1, std::min(tune().sort_tile_items, ermc_dev::sort_max_tile_items()) / R);
   s->d_counters.ensure(2 * std::max<int64_t>(n_chunks, 1));
   s->d_errcode.ensure(std::max<int64_t>(n_chunks, 1));
   cuda_check(cudaMemsetAsync(s->d_counters.p, 0,
@@ -862,6 +888,7 @@ void set_field_impl(ermc_session* s, const double* t, int is_device,
   s->d_levels32.clear();
   s->d_field32.reset();
   s->d_field32b.reset();
+  s->d_field64b.reset();
 }
 
 void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
@@ -942,7 +969,16 @@ int solve_host(const ermc_grid_t* grid, const double* temperature,
   return guarded(errbuf, errlen, [&] {
     const auto t0 = std::chrono::steady_clock::now();
     if (!out) throw Error("ermc_b200: null solution");
+    // ERMC_HOST_PROFILE=1: phase times of this call on stderr (diagnostics).
+    static const bool prof = env_int("ERMC_HOST_PROFILE", 0) != 0;
+    auto mark = [&](const char* what) {
+      if (!prof) return;
+      std::fprintf(stderr, "ermc_b200 solve_host: %-12s %9.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(
+                       std::chrono::steady_clock::now() - t0).count());
+    };
     std::unique_ptr<ermc_session> s(create_session(grid, boundary, model, config));
+    mark("session");
     DeviceGuard guard(s->device);
     cudaStream_t st;
     cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
@@ -951,11 +987,14 @@ int solve_host(const ermc_grid_t* grid, const double* temperature,
       ~StreamGuard() { cudaStreamDestroy(s); }
     } sg{st};
     set_field_impl(s.get(), temperature, 0, st);
+    if (prof) cudaStreamSynchronize(st);
+    mark("h2d field");
     const int64_t n = hi - lo;
     DevBuf<double> dq, dsd;
     dq.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
     dsd.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
     session_solve_impl(s.get(), lo, hi, dq.p, dsd.p, out->steps_per_level, st);
+    mark("solve");
     if (n > 0) {
       cuda_check(cudaMemcpyAsync(out->q_r, dq.p, n * sizeof(double),
                                  cudaMemcpyDeviceToHost, st), "D2H q_r");
@@ -963,6 +1002,7 @@ int solve_host(const ermc_grid_t* grid, const double* temperature,
                                  cudaMemcpyDeviceToHost, st), "D2H std_dev");
     }
     cuda_check(cudaStreamSynchronize(st), "sync");
+    mark("d2h q, sigma");
     int64_t total = 0;
     for (int l = 0; l < config->n_levels; ++l) total += out->steps_per_level[l];
     out->total_steps = total;

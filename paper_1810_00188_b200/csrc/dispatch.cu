@@ -27,57 +27,74 @@
 
 namespace ermc_dev {
 
-constexpr int kSortBlock = 256;
+constexpr int kSortBlock = 512;
 constexpr int kMaxSortBins = 8192;  // >= the 8001 rows of a line-by-line model
 
 namespace {
 
-__device__ __forceinline__ uint32_t work_key(const TraceParams& P,
-                                             const int32_t* __restrict__ row_rank,
-                                             uint32_t w) {
-  const uint32_t rays = static_cast<uint32_t>(P.rays);
-  const uint32_t c = w / rays;
-  const uint32_t ray = w - c * rays;
-  const uint64_t h_cell =
-      mix64(P.h_seed ^ static_cast<uint64_t>(P.cell_base + static_cast<int64_t>(c)));
-  int n, g;
-  sample_band(P, draw_u(h_cell, ray, 2), draw_u(h_cell, ray, 3), n, g);
-  return static_cast<uint32_t>(__ldg(row_rank + n * P.n_quad + g));
+// std::upper_bound (sampling.cpp:44-51) over a CDF in shared or global memory.
+__device__ __forceinline__ int upper_bound_any(const double* a, int n, double x) {
+  int first = 0, count = n;
+  while (count > 0) {
+    const int step = count >> 1;
+    if (!(x < a[first + step])) {
+      first += step + 1;
+      count -= step + 1;
+    } else {
+      count = step;
+    }
+  }
+  return first;
 }
 
-// One block per spatial tile of `tile_cells` whole cells (tile_cells * R
-// work ids). The sort is local to the tile: keys, histogram, scan and
-// scatter all stay in shared memory and the tile's own slice of perm, so it
-// needs no global atomics, and the dispatch order keeps the cell-major
-// order's spatial locality — the rays in flight at any time start from a
-// couple of neighbouring tiles, so their temperature gathers share the L2
-// the way unsorted rays do — while consecutive lanes draw the same row.
+// One block per spatial tile of `tile_items` work ids (whole cells). The sort
+// is local to the tile — a shared-memory counting sort writing the tile's
+// own slice of perm — so it needs no global atomics, and the dispatch order
+// keeps the cell-major order's spatial locality: the rays in flight at any
+// time start from a couple of neighbouring tiles, so their temperature
+// gathers share the L2 the way unsorted rays do, while consecutive lanes
+// draw the same spectral row.
+//   pass 1: key and the item's rank inside its bin (the shared atomic's old
+//           value), packed as key << 16 | rank (tile_items <= 2^16);
+//   scan:   bin offsets;
+//   pass 2: perm[tile + offset[key] + rank] = id — no atomics.
+// Dynamic shared memory: n_bins counters, kSortBlock partial sums, and the
+// band / g CDFs when they fit (cdf_len > 0).
 __global__ void __launch_bounds__(kSortBlock)
     ng_tile_sort(const __grid_constant__ TraceParams P, const int32_t* __restrict__ row_rank,
-                 int n_bins, uint32_t tile_items, uint16_t* __restrict__ keys,
+                 int n_bins, int cdf_len, uint32_t tile_items, uint32_t* __restrict__ packed,
                  uint32_t* __restrict__ perm) {
-  __shared__ unsigned int s_cur[kMaxSortBins];
-  __shared__ unsigned int s_part[kSortBlock];
-  const unsigned lane = threadIdx.x & 31u;
-  const unsigned lt = (1u << lane) - 1u;
+  extern __shared__ __align__(8) unsigned char s_raw[];
+  double* s_cdf = reinterpret_cast<double*>(s_raw);
+  unsigned int* s_cur = reinterpret_cast<unsigned int*>(s_raw + cdf_len * sizeof(double));
+  unsigned int* s_part = s_cur + n_bins;
   const uint32_t n = static_cast<uint32_t>(P.n_work);
   const uint32_t t0 = blockIdx.x * tile_items;
   const uint32_t t1 = min(n, t0 + tile_items);
+  const int nb = P.n_bands, nq = P.n_quad;
   for (int b = threadIdx.x; b < n_bins; b += blockDim.x) s_cur[b] = 0u;
+  for (int b = threadIdx.x; b < cdf_len; b += blockDim.x)
+    s_cdf[b] = b < nb ? P.band_cdf[b] : P.quad_cdf[b - nb];
   __syncthreads();
-  // keys + histogram (warp-aggregated shared atomics: hot rows are common)
-  for (uint32_t base = t0; base < t1; base += blockDim.x) {
-    const uint32_t w = base + threadIdx.x;
-    const bool valid = w < t1;
-    const unsigned key = valid ? work_key(P, row_rank, w) : 0xffffffffu;
-    const unsigned peers = __match_any_sync(kFullMask, key);
-    if (valid) {
-      keys[w] = static_cast<uint16_t>(key);
-      if (lane == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&s_cur[key], __popc(peers));
-    }
+  const double* band_cdf = cdf_len ? s_cdf : P.band_cdf;
+  const double* quad_cdf = cdf_len ? s_cdf + nb : P.quad_cdf;
+  const uint32_t rays = static_cast<uint32_t>(P.rays);
+  for (uint32_t w = t0 + threadIdx.x; w < t1; w += blockDim.x) {
+    // sample_band on draws 2 and 3 of the ray's key (sampling.cpp:42-53, 77-78)
+    const uint32_t c = w / rays;
+    const uint32_t ray = w - c * rays;
+    const uint64_t h_cell =
+        mix64(P.h_seed ^ static_cast<uint64_t>(P.cell_base + static_cast<int64_t>(c)));
+    int bn = upper_bound_any(band_cdf, nb, draw_u(h_cell, ray, 2));
+    if (bn >= nb) bn = nb - 1;
+    int g = upper_bound_any(quad_cdf + bn * nq, nq, draw_u(h_cell, ray, 3));
+    if (g >= nq) g = nq - 1;
+    const unsigned key = static_cast<unsigned>(__ldg(row_rank + bn * nq + g));
+    const unsigned rank = atomicAdd(&s_cur[key], 1u);
+    packed[w] = key << 16 | rank;
   }
   __syncthreads();
-  // exclusive scan of the histogram in place: per-thread segments, then a
+  // exclusive scan of the counts in place: per-thread segments, then a
   // serial scan of the kSortBlock segment sums
   const int per = (n_bins + kSortBlock - 1) / kSortBlock;
   const int b0 = threadIdx.x * per;
@@ -102,32 +119,34 @@ __global__ void __launch_bounds__(kSortBlock)
     run += v;
   }
   __syncthreads();
-  // scatter into the tile's slice of perm (ascending ids inside a warp)
-  for (uint32_t base = t0; base < t1; base += blockDim.x) {
-    const uint32_t w = base + threadIdx.x;
-    const bool valid = w < t1;
-    const unsigned key = valid ? keys[w] : 0xffffffffu;
-    const unsigned peers = __match_any_sync(kFullMask, key);
-    const int leader = __ffs(peers) - 1;
-    unsigned int pos = 0;
-    if (valid && static_cast<int>(lane) == leader) pos = atomicAdd(&s_cur[key], __popc(peers));
-    pos = __shfl_sync(kFullMask, pos, leader);
-    if (valid) perm[t0 + pos + __popc(peers & lt)] = w;
+  for (uint32_t w = t0 + threadIdx.x; w < t1; w += blockDim.x) {
+    const uint32_t kr = packed[w];
+    perm[t0 + s_cur[kr >> 16] + (kr & 0xffffu)] = w;
   }
 }
 
 }  // namespace
 
 int sort_max_bins() { return kMaxSortBins; }
+int sort_max_tile_items() { return 1 << 16; }
 
 cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_bins,
-                           int tile_cells, uint16_t* keys, uint32_t* perm, cudaStream_t s) {
+                           int tile_cells, uint32_t* packed, uint32_t* perm, cudaStream_t s) {
   if (P.n_work == 0) return cudaSuccess;
-  if (n_bins > kMaxSortBins) return cudaErrorInvalidValue;
   const uint32_t tile_items = static_cast<uint32_t>(tile_cells) * static_cast<uint32_t>(P.rays);
+  if (n_bins > kMaxSortBins || tile_items > (1u << 16)) return cudaErrorInvalidValue;
+  const int cdf_total = P.n_bands + P.n_bands * P.n_quad;
+  const int cdf_len = cdf_total <= 4096 ? cdf_total : 0;
+  const size_t smem = cdf_len * sizeof(double) + (n_bins + kSortBlock) * sizeof(unsigned int);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        ng_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
   const uint32_t n = static_cast<uint32_t>(P.n_work);
   const uint32_t tiles = (n + tile_items - 1) / tile_items;
-  ng_tile_sort<<<tiles, kSortBlock, 0, s>>>(P, row_rank, n_bins, tile_items, keys, perm);
+  ng_tile_sort<<<tiles, kSortBlock, smem, s>>>(P, row_rank, n_bins, cdf_len, tile_items,
+                                               packed, perm);
   return cudaGetLastError();
 }
 

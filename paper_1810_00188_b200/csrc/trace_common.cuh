@@ -24,6 +24,7 @@ struct LevelDesc {
   const double* field;   // fp64 temperature, k-fastest
   const float* field32;  // fp32 copy for the fast kernel (may be null)
   const float* field32b;   // fp32 in 2x2x2 micro-bricks (even grids, lean kernel)
+  const double* field64b;  // fp64 in 2x2x2 micro-bricks (even grids, lean kernel)
 };
 
 // Error codes raised on the device; the host re-traces the failing ray
@@ -85,7 +86,7 @@ struct TraceParams {
   int32_t inner_steps;       // march steps between two pool checks
   int32_t lean;              // fp64: 1 = lean tracer (per-axis records in smem)
   int32_t cache_hint;        // L1 policy of the lean tracers' loads (0, 1, 2)
-  int32_t brick;             // fp32 lean tracer reads the micro-brick field copy
+  int32_t brick;             // lean tracers read the micro-brick field copy
   int64_t cell_base;         // first global linear cell of this chunk
   int64_t n_cells;           // cells in this chunk
   uint64_t n_work;           // n_cells * rays (ray work items)

@@ -687,9 +687,15 @@ __device__ __forceinline__ double expm1_lean(double x) {
 //   ax[a] = {t_delta (lo, hi words), signed linear stride, cells left before
 //            the domain face (or the fixed index of a non-moving axis)}.
 // rec[3] = {band, next_draw, cell id, ray id}: state only walls touch.
+// kBrick: the temperature gathers read the 2x2x2 micro-brick copy of the
+// field (64 bytes per brick, even grids; brick_index in device_common.cuh);
+// the stride word then holds the signed index delta of a step that leaves
+// the brick ("far"), and the in-brick delta is +-(4 >> axis) with far's sign.
+// A step leaves its brick exactly when the cells-left counter is even before
+// the step (either direction, even n).
 constexpr int kLeanRecs64 = 4;
 
-template <int kHint>
+template <int kHint, bool kBrick>
 struct Fp64Lean {
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
@@ -706,7 +712,9 @@ struct Fp64Lean {
 
   // Dda::setup (tracer.cpp:17-38) + the per-axis records.
   __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx) {
-    const int stride[3] = {L.n[1] * L.n[2], L.n[2], 1};
+    const int nby = (L.n[1] + 1) >> 1, nbz = (L.n[2] + 1) >> 1;
+    const int stride[3] = {kBrick ? 8 * nby * nbz - 4 : L.n[1] * L.n[2],
+                           kBrick ? 8 * nbz - 2 : L.n[2], kBrick ? 7 : 1};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double da = dir[a];
@@ -724,7 +732,8 @@ struct Fp64Lean {
                                  pos_dir ? stride[a] : -stride[a],
                                  pos_dir ? L.n[a] - 1 - idx[a] : idx[a]);
     }
-    lin = (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
+    lin = kBrick ? brick_index(L, idx[0], idx[1], idx[2])
+                 : (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
   }
 
   __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
@@ -784,10 +793,24 @@ struct Fp64Lean {
     const int left = rec.w - 1;
     const bool inside = left >= 0;
     const bool periodic = (P.periodic_mask >> axis) & 1;
-    int nlin = lin + rec.z;
-    if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
+    int nlin;
+    if (kBrick) {
+      const int near = rec.z > 0 ? (4 >> axis) : -(4 >> axis);
+      nlin = lin + ((rec.w & 1) ? near : rec.z);
+      if (!inside) {  // periodic image: re-index the wrapped cell
+        int idx[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          idx[a] = a == axis ? (rec.z > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
+        nlin = brick_index(L, idx[0], idx[1], idx[2]);
+      }
+    } else {
+      nlin = lin + rec.z;
+      if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
+    }
     double t_next = t_cur;
-    if (inside || periodic) t_next = ld_t64<kHint>(L.field + nlin);
+    if (inside || periodic)
+      t_next = ld_t64<kHint>((kBrick ? L.field64b : L.field) + nlin);
 
     const double kappa = frac == 0.0 ? v.x : v.x + frac * (v.y - v.x);
     const double ib2 = frac == 0.0 ? v.z : v.z + frac * (v.w - v.z);
@@ -932,10 +955,26 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     pool_kernel_body<Fp64Fast, false>(P);
 }
 
-template <int kMinBlocks, int kHint>
+template <int kMinBlocks, int kHint, bool kBrick>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp64Lean<kHint>, false>(P);
+  pool_kernel_body<Fp64Lean<kHint, kBrick>, false>(P);
+}
+
+// Copies the fp64 k-fastest field into the 2x2x2 micro-brick layout.
+__global__ void to_bricked64(const double* __restrict__ src, double* __restrict__ dst,
+                             int nx, int ny, int nz) {
+  const int64_t n = static_cast<int64_t>(nx) * ny * nz;
+  const int nby = (ny + 1) >> 1, nbz = (nz + 1) >> 1;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < n;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(c / (static_cast<int64_t>(ny) * nz));
+    const int j = static_cast<int>((c / nz) % ny);
+    const int k = static_cast<int>(c % nz);
+    const int64_t b = ((static_cast<int64_t>(i >> 1) * nby + (j >> 1)) * nbz + (k >> 1)) * 8 +
+                      ((i & 1) << 2) + ((j & 1) << 1) + (k & 1);
+    dst[b] = src[c];
+  }
 }
 
 // Debug/test kernel: one thread traces one explicit ray with full
@@ -1145,9 +1184,13 @@ size_t fp64_smem(const TraceParams& P) {
 }
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
-  return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0>
-         : min_blocks == 6 ? trace_pool_fp64_lean<6, 0>
-                           : trace_pool_fp64_lean<5, 0>;
+  if (P.brick && P.lv[0].field64b)
+    return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, true>
+           : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, true>
+                             : trace_pool_fp64_lean<5, 0, true>;
+  return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, false>
+         : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, false>
+                           : trace_pool_fp64_lean<5, 0, false>;
 }
 TraceFn fp64_kernel(bool multi, int min_blocks) {
   if (multi) return min_blocks >= 5 ? trace_pool_fp64<true, 5> : trace_pool_fp64<true, 4>;
@@ -1217,6 +1260,16 @@ cudaError_t launch_field_stats(const double* t, int64_t n, double* scratch,
   auto* pbad = reinterpret_cast<unsigned long long*>(scratch + 2 * n_blocks);
   field_stats_partial<<<n_blocks, 256, 0, stream>>>(t, n, pmin, pmax, pbad);
   field_stats_final<<<1, 32, 0, stream>>>(pmin, pmax, pbad, n_blocks, out3);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_bricked64(const double* src, double* dst, int nx, int ny, int nz,
+                                cudaStream_t stream) {
+  const int64_t n = static_cast<int64_t>(nx) * ny * nz;
+  if (n <= 0) return cudaSuccess;
+  const int64_t want = (n + 255) / 256;
+  to_bricked64<<<static_cast<unsigned>(want < 4096 ? want : 4096), 256, 0, stream>>>(
+      src, dst, nx, ny, nz);
   return cudaGetLastError();
 }
 
