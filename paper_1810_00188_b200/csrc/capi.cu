@@ -272,13 +272,14 @@ struct Timing {
 // Scheduling knobs (defaults tuned on B200; ERMC_* environment variables
 // override them for experiments — they never change results).
 struct Tune {
-  int inner_steps = 16;
+  int inner_steps = 32;
   int refill = 8;
   int fp64_min_blocks = 6;
-  int fp32_min_blocks = 6;
+  int fp32_min_blocks = 8;
   int lean = 1;
   int cache_hint = 0;
-  int brick = 1;
+  int brick = 1;    // fp32: micro-brick field copy (measured +4 %)
+  int brick64 = 0;  // fp64: micro-brick field copy (measured neutral; off saves 8 B/cell)
   int sort = 1;  // narrow-band sorted dispatch (dispatch.cu)
   int sort_tile_items = 1 << 16;
 };
@@ -296,6 +297,7 @@ const Tune& tune() {
     x.lean = env_int("ERMC_LEAN", x.lean);
     x.cache_hint = env_int("ERMC_CACHE_HINT", x.cache_hint);
     x.brick = env_int("ERMC_BRICK", x.brick);
+    x.brick64 = env_int("ERMC_BRICK64", x.brick64);
     x.sort = env_int("ERMC_SORT", x.sort);
     x.sort_tile_items = std::max(1, env_int("ERMC_SORT_TILE", x.sort_tile_items));
     return x;
@@ -718,7 +720,7 @@ void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
 void ensure_fp64_brick(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t st) {
   const ermc_grid_t& g0 = s->grid;
   const bool even = g0.nx % 2 == 0 && g0.ny % 2 == 0 && g0.nz % 2 == 0;
-  P.brick = (tune().brick && even && s->config.n_levels == 1 &&
+  P.brick = (tune().brick64 && even && s->config.n_levels == 1 &&
              s->n_cells < (int64_t(1) << 31)) ? 1 : 0;
   if (!P.brick) return;
   if (!s->d_field64b.p) {

@@ -518,6 +518,7 @@ struct Fp32Lean {
 //            {inf, INT_MAX, 0, fixed index}                 (non-moving axis).
 // With even n a step leaves its brick exactly when the cells-left counter is
 // even before the step, for either direction.
+template <int kHint>
 struct Fp32Brick {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
@@ -606,7 +607,7 @@ struct Fp32Brick {
     const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
     const int lo = min(static_cast<int>(u), P.n_temps - 2);
     const float f = u - static_cast<float>(lo);
-    const float4 v = __ldg(row + lo);
+    const float4 v = ld_rec32<kHint>(row + lo);
 
     int axis = 0;
     float tmin = tn[0];
@@ -633,14 +634,14 @@ struct Fp32Brick {
     int nlin = lin + ((r.y & 1) ? r.z : r.w);
     float t_next = t_cur;
     if (inside) {
-      t_next = __ldg(L.field32b + nlin);
+      t_next = ld_t32<kHint>(L.field32b + nlin);
     } else if (periodic) {
       int idx[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
         idx[a] = a == axis ? (r.z > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
       nlin = brick_index(L, idx[0], idx[1], idx[2]);
-      t_next = __ldg(L.field32b + nlin);
+      t_next = ld_t32<kHint>(L.field32b + nlin);
     }
 
     const float kappa = fmaf(f, v.y, v.x);
@@ -727,10 +728,10 @@ struct Fp32Brick {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-template <int kMinBlocks>
+template <int kMinBlocks, int kHint>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp32Brick, false>(P);
+  pool_kernel_body<Fp32Brick<kHint>, false>(P);
 }
 
 // Converts the fp64 k-fastest field to the fp32 micro-brick layout.
@@ -807,8 +808,11 @@ size_t fp32_smem(const TraceParams& P) {
   return fp32_lean(P) ? 3 * kBlock32 * sizeof(int4) : 0;
 }
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
-  if (fp32_lean(P) && P.brick)
-    return min_blocks >= 8 ? trace_pool_fp32_brick<8> : trace_pool_fp32_brick<6>;
+  if (fp32_lean(P) && P.brick) {
+    if (P.cache_hint == 1) return trace_pool_fp32_brick<6, 1>;
+    if (P.cache_hint == 2) return trace_pool_fp32_brick<6, 2>;
+    return min_blocks >= 8 ? trace_pool_fp32_brick<8, 0> : trace_pool_fp32_brick<6, 0>;
+  }
   if (fp32_lean(P))
     return min_blocks >= 8 ? trace_pool_fp32_lean<8, 0> : trace_pool_fp32_lean<6, 0>;
   return min_blocks >= 8 ? trace_pool_fp32<8> : trace_pool_fp32<6>;

@@ -1184,6 +1184,12 @@ size_t fp64_smem(const TraceParams& P) {
 }
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
+  if (P.cache_hint == 1)
+    return P.brick && P.lv[0].field64b ? trace_pool_fp64_lean<6, 1, true>
+                                       : trace_pool_fp64_lean<6, 1, false>;
+  if (P.cache_hint == 2)
+    return P.brick && P.lv[0].field64b ? trace_pool_fp64_lean<6, 2, true>
+                                       : trace_pool_fp64_lean<6, 2, false>;
   if (P.brick && P.lv[0].field64b)
     return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, true>
            : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, true>
