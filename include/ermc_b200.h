@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define ERMC_B200_ABI_VERSION 1
+#define ERMC_B200_ABI_VERSION 2
 
 /* CartesianGrid (reference geometry.hpp:13-36). */
 typedef struct ermc_grid {
@@ -86,6 +86,14 @@ typedef struct ermc_config {
   int32_t workers;   /* accepted and validated (>= 0); the GPU ignores it */
   int32_t precision; /* ERMC_PRECISION_* */
   int32_t device;    /* CUDA ordinal, -1 = current */
+  /* One-shot solves (ermc_b200_solve / _solve_range) split their cell range
+   * into n_devices contiguous parts solved concurrently, part p on device
+   * (device + p) mod (visible devices), each with a replicated T field —
+   * the GPU form of the reference's worker chunks (solver.cpp:159-170).
+   * Results are byte-identical for any n_devices. 0 or 1 = one device.
+   * Sessions always use one device. */
+  int32_t n_devices;
+  int32_t reserved0;
 } ermc_config_t;
 
 /* Fills the reference SolveConfig defaults (solver.hpp:12-26). */

@@ -234,6 +234,7 @@ struct SolveConfig {
   // B200 extensions (defaults keep reference semantics):
   Precision precision = Precision::fp64;
   int device = -1;  // CUDA ordinal, -1 = current device
+  int n_devices = 1;  // GPUs one solve spreads over (ermc_config_t::n_devices)
 
   void validate() const;
   ermc_config_t c_view() const;

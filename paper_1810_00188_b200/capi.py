@@ -47,7 +47,8 @@ class Config(C.Structure):
                 ("max_steps", C.c_int64), ("sorting", C.c_int32),
                 ("steps_per_level", C.c_int32), ("coarsen_ratio", C.c_int32),
                 ("volume_sampling", C.c_int32), ("specular_walls", C.c_int32),
-                ("workers", C.c_int32), ("precision", C.c_int32), ("device", C.c_int32)]
+                ("workers", C.c_int32), ("precision", C.c_int32), ("device", C.c_int32),
+                ("n_devices", C.c_int32), ("reserved0", C.c_int32)]
 
 
 class Solution(C.Structure):
@@ -198,7 +199,7 @@ def default_config_values() -> dict:
     library (used by CPU tests)."""
     return dict(rays_per_cell=2000, n_levels=1, tolerance=1e-4, seed=0, max_steps=100000,
                 sorting=0, steps_per_level=5, coarsen_ratio=2, volume_sampling=0,
-                specular_walls=0, workers=0, precision=FP64, device=-1)
+                specular_walls=0, workers=0, precision=FP64, device=-1, n_devices=1)
 
 
 def config_struct(**kw) -> Config:

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <map>
 #include <string>
@@ -230,6 +231,7 @@ void validate_config(const ermc_config_t& c) {
   if (c.workers < 0) throw Error("SolveConfig: workers must be >= 0");
   if (c.precision != ERMC_PRECISION_FP64 && c.precision != ERMC_PRECISION_FP32)
     throw Error("SolveConfig: precision must be fp64 (0) or fp32 (1)");
+  if (c.n_devices < 0) throw Error("ermc_b200: n_devices must be >= 0");
   if (c.n_levels > ermc_dev::kMaxLevels)
     throw Error("SolveConfig: n_levels above the GPU limit of " +
                 std::to_string(ermc_dev::kMaxLevels));
@@ -272,7 +274,8 @@ struct Timing {
 // Scheduling knobs (defaults tuned on B200; ERMC_* environment variables
 // override them for experiments — they never change results).
 struct Tune {
-  int inner_steps = 32;
+  int inner_steps = 32;    // fp64 march steps per pool check
+  int inner_steps32 = 64;  // fp32
   int refill = 8;
   int fp64_min_blocks = 6;
   int fp32_min_blocks = 8;
@@ -281,6 +284,7 @@ struct Tune {
   int brick = 1;    // fp32: micro-brick field copy (measured +4 %)
   int brick64 = 0;  // fp64: micro-brick field copy (measured neutral; off saves 8 B/cell)
   int sort = 1;  // narrow-band sorted dispatch (dispatch.cu)
+  int track_pos = 0;  // 1 forces the position-tracking fp64 kernel
   int sort_tile_items = 1 << 16;
 };
 int env_int(const char* name, int fallback) {
@@ -291,6 +295,7 @@ const Tune& tune() {
   static const Tune t = [] {
     Tune x;
     x.inner_steps = std::max(1, env_int("ERMC_INNER_STEPS", x.inner_steps));
+    x.inner_steps32 = std::max(1, env_int("ERMC_INNER_STEPS32", x.inner_steps32));
     x.refill = std::max(1, std::min(32, env_int("ERMC_REFILL", x.refill)));
     x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
@@ -299,6 +304,7 @@ const Tune& tune() {
     x.brick = env_int("ERMC_BRICK", x.brick);
     x.brick64 = env_int("ERMC_BRICK64", x.brick64);
     x.sort = env_int("ERMC_SORT", x.sort);
+    x.track_pos = env_int("ERMC_TRACK_POS", x.track_pos);
     x.sort_tile_items = std::max(1, env_int("ERMC_SORT_TILE", x.sort_tile_items));
     return x;
   }();
@@ -665,6 +671,13 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.t_first = v.temps[0];
   P.t_last = v.temps[v.nt - 1];
   P.steps_per_level = s->d_steps.p;
+  // Positions matter after a wall only if some wall can reflect.
+  P.track_pos = 0;
+  for (int a = 0; a < 3; ++a)
+    if (b.kind[a] != ERMC_AXIS_PERIODIC &&
+        (b.lo_emissivity[a] != 1.0 || b.hi_emissivity[a] != 1.0))
+      P.track_pos = 1;
+  if (tune().track_pos) P.track_pos = 1;
 }
 
 double q_emission(const ermc_session* s, double t_max) {
@@ -750,8 +763,10 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
   prepare(s, pr, t_max, qe, /*build_levels=*/true, st);
   ermc_dev::TraceParams& P = pr.P;
   const bool fp32 = s->config.precision == ERMC_PRECISION_FP32;
-  if (fp32)
+  if (fp32) {
+    P.inner_steps = tune().inner_steps32;
     ensure_fp32_inputs(s, P, st);
+  }
   else
     ensure_fp64_brick(s, P, st);
 
@@ -963,7 +978,56 @@ int guarded(char* errbuf, size_t errlen, F&& f) {
   }
 }
 
-// Pinned staging for the host-buffer entry points (H2D of T, D2H of Q_r).
+// One part of a one-shot solve on config->device: session, H2D of the whole
+// T field (replicated per device), solve of [lo, hi), D2H of Q_r / sigma
+// into q_out / sd_out. Throws ermc::Error.
+void solve_part(const ermc_grid_t* grid, const double* temperature,
+                const ermc_boundary_t* boundary, const ermc_model_t* model,
+                const ermc_config_t* config, int64_t lo, int64_t hi, double* q_out,
+                double* sd_out, int64_t* steps_out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  // ERMC_HOST_PROFILE=1: phase times of this call on stderr (diagnostics).
+  static const bool prof = env_int("ERMC_HOST_PROFILE", 0) != 0;
+  auto mark = [&](const char* what) {
+    if (!prof) return;
+    std::fprintf(stderr, "ermc_b200 solve_host: %-12s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(
+                     std::chrono::steady_clock::now() - t0).count());
+  };
+  std::unique_ptr<ermc_session> s(create_session(grid, boundary, model, config));
+  mark("session");
+  DeviceGuard guard(s->device);
+  cudaStream_t st;
+  cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{st};
+  set_field_impl(s.get(), temperature, 0, st);
+  if (prof) cudaStreamSynchronize(st);
+  mark("h2d field");
+  const int64_t n = hi - lo;
+  DevBuf<double> dq, dsd;
+  dq.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  dsd.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  session_solve_impl(s.get(), lo, hi, dq.p, dsd.p, steps_out, st);
+  mark("solve");
+  if (n > 0) {
+    cuda_check(cudaMemcpyAsync(q_out, dq.p, n * sizeof(double), cudaMemcpyDeviceToHost, st),
+               "D2H q_r");
+    cuda_check(cudaMemcpyAsync(sd_out, dsd.p, n * sizeof(double), cudaMemcpyDeviceToHost, st),
+               "D2H std_dev");
+  }
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  mark("d2h q, sigma");
+}
+
+// Host-buffer entry points (ermc_b200_solve / _solve_range): the range is
+// split into config->n_devices contiguous parts solved concurrently, one
+// host thread per part (the reference's worker chunks, solver.cpp:159-170,
+// with a GPU per chunk). Each cell is computed identically wherever it runs,
+// so the result does not depend on the split. The error reported is the one
+// of the lowest failing part — the cells a single worker reaches first.
 int solve_host(const ermc_grid_t* grid, const double* temperature,
                const ermc_boundary_t* boundary, const ermc_model_t* model,
                const ermc_config_t* config, int64_t lo, int64_t hi,
@@ -971,42 +1035,54 @@ int solve_host(const ermc_grid_t* grid, const double* temperature,
   return guarded(errbuf, errlen, [&] {
     const auto t0 = std::chrono::steady_clock::now();
     if (!out) throw Error("ermc_b200: null solution");
-    // ERMC_HOST_PROFILE=1: phase times of this call on stderr (diagnostics).
-    static const bool prof = env_int("ERMC_HOST_PROFILE", 0) != 0;
-    auto mark = [&](const char* what) {
-      if (!prof) return;
-      std::fprintf(stderr, "ermc_b200 solve_host: %-12s %9.3f ms\n", what,
-                   std::chrono::duration<double, std::milli>(
-                       std::chrono::steady_clock::now() - t0).count());
-    };
-    std::unique_ptr<ermc_session> s(create_session(grid, boundary, model, config));
-    mark("session");
-    DeviceGuard guard(s->device);
-    cudaStream_t st;
-    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
-    struct StreamGuard {
-      cudaStream_t s;
-      ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{st};
-    set_field_impl(s.get(), temperature, 0, st);
-    if (prof) cudaStreamSynchronize(st);
-    mark("h2d field");
-    const int64_t n = hi - lo;
-    DevBuf<double> dq, dsd;
-    dq.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
-    dsd.ensure(static_cast<size_t>(std::max<int64_t>(n, 1)));
-    session_solve_impl(s.get(), lo, hi, dq.p, dsd.p, out->steps_per_level, st);
-    mark("solve");
-    if (n > 0) {
-      cuda_check(cudaMemcpyAsync(out->q_r, dq.p, n * sizeof(double),
-                                 cudaMemcpyDeviceToHost, st), "D2H q_r");
-      cuda_check(cudaMemcpyAsync(out->std_dev, dsd.p, n * sizeof(double),
-                                 cudaMemcpyDeviceToHost, st), "D2H std_dev");
+    if (!config) throw Error("ermc_b200: null descriptor");
+    if (config->n_devices < 0) throw Error("ermc_b200: n_devices must be >= 0");
+    const int parts = std::max(1, config->n_devices);
+    const int n_levels = std::max(1, config->n_levels);
+    std::vector<int64_t> steps(static_cast<size_t>(parts) * n_levels, 0);
+    if (parts == 1) {
+      solve_part(grid, temperature, boundary, model, config, lo, hi, out->q_r, out->std_dev,
+                 steps.data());
+    } else {
+      int n_dev = 0;
+      if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+        cudaGetLastError();
+        throw Error("ermc_b200: no CUDA device available (the solver has no CPU path)");
+      }
+      int base = config->device;
+      if (base < 0) cuda_check(cudaGetDevice(&base), "cudaGetDevice");
+      if (base >= n_dev) throw Error("ermc_b200: device ordinal out of range");
+      const int64_t n = hi - lo;
+      std::vector<std::string> errors(parts);
+      std::vector<std::thread> pool;
+      for (int p = 0; p < parts; ++p) {
+        const int64_t a = lo + n * p / parts, b = lo + n * (p + 1) / parts;
+        pool.emplace_back([&, p, a, b] {
+          try {
+            ermc_config_t c = *config;
+            c.device = (base + p) % n_dev;
+            c.n_devices = 1;
+            solve_part(grid, temperature, boundary, model, &c, a, b, out->q_r + (a - lo),
+                       out->std_dev + (a - lo), steps.data() + static_cast<size_t>(p) * n_levels);
+          } catch (const std::exception& e) {
+            errors[p] = e.what();
+            if (errors[p].empty()) errors[p] = "ermc_b200: unknown error";
+          } catch (...) {
+            errors[p] = "ermc_b200: unknown error";
+          }
+        });
+      }
+      for (auto& t : pool) t.join();
+      for (const std::string& e : errors)
+        if (!e.empty()) throw Error(e);
     }
-    cuda_check(cudaStreamSynchronize(st), "sync");
-    mark("d2h q, sigma");
     int64_t total = 0;
-    for (int l = 0; l < config->n_levels; ++l) total += out->steps_per_level[l];
+    for (int l = 0; l < n_levels; ++l) {
+      int64_t v = 0;
+      for (int p = 0; p < parts; ++p) v += steps[static_cast<size_t>(p) * n_levels + l];
+      out->steps_per_level[l] = v;
+      total += v;
+    }
     out->total_steps = total;
     out->wall_time = std::chrono::duration<double>(
                          std::chrono::steady_clock::now() - t0).count();
@@ -1025,6 +1101,7 @@ void ermc_b200_config_default(ermc_config_t* c) {
   c->seed = 0;
   c->max_steps = 100000;
   c->sorting = 0;
+  c->n_devices = 1;
   c->steps_per_level = 5;
   c->coarsen_ratio = 2;
   c->volume_sampling = 0;

@@ -483,6 +483,7 @@ ermc_config_t SolveConfig::c_view() const {
   c.workers = workers;
   c.precision = static_cast<int32_t>(precision);
   c.device = device;
+  c.n_devices = n_devices;
   return c;
 }
 

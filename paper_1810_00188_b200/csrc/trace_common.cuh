@@ -87,6 +87,7 @@ struct TraceParams {
   int32_t lean;              // fp64: 1 = lean tracer (per-axis records in smem)
   int32_t cache_hint;        // L1 policy of the lean tracers' loads (0, 1, 2)
   int32_t brick;             // lean tracers read the micro-brick field copy
+  int32_t track_pos;         // 0 when every wall is black (positions never read)
   int64_t cell_base;         // first global linear cell of this chunk
   int64_t n_cells;           // cells in this chunk
   uint64_t n_work;           // n_cells * rays (ray work items)

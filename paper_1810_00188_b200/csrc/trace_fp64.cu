@@ -693,9 +693,12 @@ __device__ __forceinline__ double expm1_lean(double x) {
 // the brick ("far"), and the in-brick delta is +-(4 >> axis) with far's sign.
 // A step leaves its brick exactly when the cells-left counter is even before
 // the step (either direction, even n).
+// kPos = false when every wall is black: a ray that reaches a wall then ends
+// there (tau *= 1 - 1), so its position is never read again after init and
+// the per-step position update (3 multiplies + 3 adds) is dead work.
 constexpr int kLeanRecs64 = 4;
 
-template <int kHint, bool kBrick>
+template <int kHint, bool kBrick, bool kPos = true>
 struct Fp64Lean {
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
@@ -820,9 +823,11 @@ struct Fp64Lean {
     tau *= 1.0 - alpha;
 
     const double advance = ds + L.eps;
-    pos[0] += advance * dir[0];
-    pos[1] += advance * dir[1];
-    pos[2] += advance * dir[2];
+    if (kPos) {
+      pos[0] += advance * dir[0];
+      pos[1] += advance * dir[1];
+      pos[2] += advance * dir[2];
+    }
     tn[0] -= advance;
     tn[1] -= advance;
     tn[2] -= advance;
@@ -842,7 +847,7 @@ struct Fp64Lean {
       const double ext = L.extent[axis];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        if (a == axis) pos[a] += rec.z > 0 ? -ext : ext;
+        if (kPos && a == axis) pos[a] += rec.z > 0 ? -ext : ext;
       lin = nlin;
       t_cur = t_next;
       return kContinue;
@@ -955,10 +960,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     pool_kernel_body<Fp64Fast, false>(P);
 }
 
-template <int kMinBlocks, int kHint, bool kBrick>
+template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp64Lean<kHint, kBrick>, false>(P);
+  pool_kernel_body<Fp64Lean<kHint, kBrick, kPos>, false>(P);
 }
 
 // Copies the fp64 k-fastest field into the 2x2x2 micro-brick layout.
@@ -1184,6 +1189,10 @@ size_t fp64_smem(const TraceParams& P) {
 }
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
+  if (!P.track_pos && !P.brick && P.cache_hint == 0)
+    return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, false, false>
+           : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, false, false>
+                             : trace_pool_fp64_lean<5, 0, false, false>;
   if (P.cache_hint == 1)
     return P.brick && P.lv[0].field64b ? trace_pool_fp64_lean<6, 1, true>
                                        : trace_pool_fp64_lean<6, 1, false>;

@@ -32,12 +32,13 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_defaults():
     lib = capi.load()
-    assert lib.ermc_b200_abi_version() == 1
+    assert lib.ermc_b200_abi_version() == 2
     c = capi.Config()
     lib.ermc_b200_config_default(ctypes.byref(c))
     assert (c.rays_per_cell, c.tolerance, c.max_steps, c.steps_per_level, c.coarsen_ratio) == \
         (2000, 1e-4, 100000, 5, 2)
-    assert c.precision == capi.FP64 and c.device == -1
+    assert c.precision == capi.FP64 and c.device == -1 and c.n_devices == 1
+    assert capi.default_config_values()["n_devices"] == 1
 
 
 def test_struct_layouts_match_header(tmp_path):

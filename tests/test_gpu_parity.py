@@ -220,3 +220,20 @@ def test_lbl_reference_matches_reference(profile):
     assert s.total_steps == r.total_steps
     assert_fp64_parity(np.asarray(s.q_r), np.asarray(r.q_r),
                        np.asarray(s.std_dev), np.asarray(r.std_dev))
+
+
+@pytest.mark.parametrize("n_devices", [2, 3])
+def test_multi_device_split_is_byte_identical(n_devices):
+    # ermc_config_t.n_devices: the range is split into contiguous parts on
+    # (device + p) mod visible devices, one host thread each. On a one-GPU box
+    # the parts share the device; the assembly and the result must not change.
+    g, t, b, m = W.channel_case(24, "nongrey16")[:4]
+    one = capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=32, seed=4))
+    many = capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=32, seed=4,
+                                                     n_devices=n_devices))
+    assert np.array_equal(one[0], many[0]) and np.array_equal(one[1], many[1])
+    assert list(one[2]) == list(many[2]) and one[3] == many[3]
+    lo, hi = 1000, 9000
+    part = capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=32, seed=4,
+                                                     n_devices=n_devices), cell_range=(lo, hi))
+    assert np.array_equal(part[0], one[0][lo:hi])
