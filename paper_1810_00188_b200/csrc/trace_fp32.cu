@@ -41,6 +41,23 @@ __device__ __forceinline__ float absorb32(float x) {
   return 1.0f - __expf(-x);
 }
 
+// locate (geometry.cpp:112-138) of a demoted ray on level C, axis a. The
+// reference nudges the position by eps * dir (1e-12 of a cell) so that a
+// ray sitting on a coarse face — every other fine face it crosses — lands in
+// the cell it is moving into; in fp32 that nudge is below resolution, so a
+// coordinate within 8 ulps of a face is resolved by the direction instead
+// (otherwise the ray would take an extra zero-length step back across it).
+__device__ __forceinline__ int locate32(const LevelDesc& C, int a, float p, float d) {
+  const float rel = (p - static_cast<float>(C.origin[a])) / static_cast<float>(C.d[a]);
+  const float fl = floorf(rel);
+  const float fr = rel - fl;
+  const float tie = 8.0f * 1.1920929e-7f * fmaxf(fabsf(rel), 1.0f);
+  int i = static_cast<int>(fl);
+  if (d > 0.0f && fr > 1.0f - tie) ++i;
+  else if (d < 0.0f && fr < tie) --i;
+  return min(max(i, 0), C.n[a] - 1);
+}
+
 struct Fp32Tracer {
   float p0[3];   // position at s = 0
   float dir[3];
@@ -162,14 +179,7 @@ struct Fp32Tracer {
         const LevelDesc& C = P.lv[lvl];
         rebase();
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const float p = fmaf(static_cast<float>(C.eps), dir[a], p0[a]);
-          const float rel = (p - static_cast<float>(C.origin[a])) /
-                            static_cast<float>(C.d[a]);
-          int i = static_cast<int>(floorf(rel));
-          i = min(max(i, 0), C.n[a] - 1);
-          idx[a] = i;
-        }
+        for (int a = 0; a < 3; ++a) idx[a] = locate32(C, a, p0[a], dir[a]);
         sal_ = 0;
         setup(C);
         t_cur = __ldg(C.field32 + lin);
@@ -312,7 +322,9 @@ struct Fp32Tracer {
 //            a non-moving axis},
 // so one LDS.128 replaces the predicated per-axis selects and param-space
 // loads of a register-only DDA; `lin` carries the cell index.
-template <int kHint>
+// kMulti: multigrid ray coarsening (tracer.cpp:91-101) with Fp32Tracer's
+// demotion arithmetic; the records and field pointer then follow the level.
+template <int kHint, bool kMulti = false>
 struct Fp32Lean {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
@@ -320,6 +332,7 @@ struct Fp32Lean {
   const float4* row;
   int4* ax;  // &s_ax[0][threadIdx.x]; axis a at ax[a * kBlock32]
   int lin, band, steps_;
+  int lvl, sal_;  // kMulti: current level, steps on it
   uint32_t next_draw, ray_id;
   uint64_t h_cell;
   int err;
@@ -383,6 +396,8 @@ struct Fp32Lean {
     row = base.row;
     band = base.band;
     steps_ = 0;
+    lvl = 0;
+    sal_ = 0;
     next_draw = base.next_draw;
     ray_id = ray;
     h_cell = base.h_cell;
@@ -391,10 +406,27 @@ struct Fp32Lean {
     return kErrNone;
   }
 
+  // Demotion to the next coarser level (Fp32Tracer::step_t's arithmetic).
+  __device__ __forceinline__ void demote(const TraceParams& P) {
+    ++lvl;
+    const LevelDesc& C = P.lv[lvl];
+    rebase();
+    int idx[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) idx[a] = locate32(C, a, p0[a], dir[a]);
+    sal_ = 0;
+    setup(C, idx);
+    t_cur = __ldg(C.field32 + lin);
+  }
+
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
     if (tau <= P.tol32) return kDone;
     if (steps_ >= max_steps) return kDone;
-    const LevelDesc& L = P.lv[0];
+    if (kMulti) {
+      const int cap = P.lv[lvl].cap;
+      if (cap >= 0 && sal_ >= cap && lvl + 1 < P.n_levels) demote(P);
+    }
+    const LevelDesc& L = P.lv[kMulti ? lvl : 0];
     // table record of the current cell (its T arrived during the last step)
     const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
     const int lo = min(static_cast<int>(u), P.n_temps - 2);
@@ -434,6 +466,7 @@ struct Fp32Lean {
     acc = fmaf(ta, ib2n - ib1n, acc);
     tau -= ta;
     ++steps_;
+    if (kMulti) ++sal_;
 
     if (inside) {
       rp->z = left;
@@ -505,8 +538,8 @@ struct Fp32Lean {
   __device__ __forceinline__ bool finite_state() const {
     return isfinite(tau) && isfinite(acc);
   }
-  __device__ __forceinline__ int level() const { return 0; }
-  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int level() const { return kMulti ? lvl : 0; }
+  __device__ __forceinline__ int sal() const { return kMulti ? sal_ : steps_; }
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
@@ -756,6 +789,13 @@ __global__ void __launch_bounds__(kBlock32, kMinBlocks)
   pool_kernel_body<Fp32Lean<kHint>, false>(P);
 }
 
+// Multigrid variant of the lean tracer (n_levels > 1).
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kBlock32, kMinBlocks)
+    trace_pool_fp32_lean_mg(const __grid_constant__ TraceParams P) {
+  pool_kernel_body<Fp32Lean<0, true>, true>(P);
+}
+
 struct Fp32Multi : Fp32Tracer {
   __device__ __forceinline__ int step(const TraceParams& P, int m) {
     return step_t<true>(P, m);
@@ -803,11 +843,13 @@ int trace_fp32_block() { return kBlock32; }
 
 namespace {
 using TraceFn32 = void (*)(TraceParams);
-bool fp32_lean(const TraceParams& P) { return P.n_levels == 1; }
+bool fp32_lean(const TraceParams& P) { return P.lean != 0; }
 size_t fp32_smem(const TraceParams& P) {
   return fp32_lean(P) ? 3 * kBlock32 * sizeof(int4) : 0;
 }
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
+  if (fp32_lean(P) && P.n_levels > 1)
+    return min_blocks >= 8 ? trace_pool_fp32_lean_mg<8> : trace_pool_fp32_lean_mg<6>;
   if (fp32_lean(P) && P.brick) {
     if (P.cache_hint == 1) return trace_pool_fp32_brick<6, 1>;
     if (P.cache_hint == 2) return trace_pool_fp32_brick<6, 2>;

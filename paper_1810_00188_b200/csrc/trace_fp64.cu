@@ -696,15 +696,21 @@ __device__ __forceinline__ double expm1_lean(double x) {
 // kPos = false when every wall is black: a ray that reaches a wall then ends
 // there (tau *= 1 - 1), so its position is never read again after init and
 // the per-step position update (3 multiplies + 3 adds) is dead work.
+// kMulti: multigrid ray coarsening (tracer.cpp:91-101): after `cap` steps on
+// a level the ray continues on the next coarser one from its current
+// position, `locate`d as in geometry.cpp:112-138; the per-axis records and
+// the field pointer are then the coarse level's.
 constexpr int kLeanRecs64 = 4;
 
-template <int kHint, bool kBrick, bool kPos = true>
+template <int kHint, bool kBrick, bool kPos = true, bool kMulti = false>
 struct Fp64Lean {
+  static_assert(!kMulti || (kPos && !kBrick), "demotion reads positions, k-fastest levels");
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
   int4* ax;
   int row;  // first interval record of (band, g) in iv64
   int lin, steps_;
+  int lvl, sal_;  // kMulti: current level, steps on it
   int err;
 
   __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
@@ -760,6 +766,8 @@ struct Fp64Lean {
     const int64_t ng = (r.krow - P.k) / P.n_temps;
     row = static_cast<int>(ng * (P.n_temps - 1));
     steps_ = 0;
+    lvl = 0;
+    sal_ = 0;
     ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
                                static_cast<int>(cell), static_cast<int>(ray));
     t_cur = __ldg(P.lv[0].field + cell);
@@ -767,10 +775,48 @@ struct Fp64Lean {
     return kErrNone;
   }
 
+  // Demotion to the next coarser level (tracer.cpp:91-101): locate the
+  // current position there (geometry.cpp:112-138), rebuild the records and
+  // load the coarse cell's temperature.
+  __device__ __forceinline__ int demote(const TraceParams& P) {
+    ++lvl;
+    const LevelDesc& C = P.lv[lvl];
+    int idx[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double p = pos[a] + C.eps * dir[a];
+      const double rel = (p - C.origin[a]) / C.d[a];
+      int i = static_cast<int>(floor(rel));
+      if (i < 0 || i >= C.n[a]) {
+        if (rel >= -1e-9 && i < 0)
+          i = 0;
+        else if (rel <= C.n[a] + 1e-9 && i >= C.n[a])
+          i = C.n[a] - 1;
+        else
+          return kErrLocate;
+      }
+      idx[a] = i;
+    }
+    sal_ = 0;
+    setup(C, idx);
+    t_cur = __ldg(C.field + lin);
+    return kErrNone;
+  }
+
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
     if (tau <= P.tol) return kDone;
     if (steps_ >= max_steps) return kDone;
-    const LevelDesc& L = P.lv[0];
+    if (kMulti) {
+      const int cap = P.lv[lvl].cap;
+      if (cap >= 0 && sal_ >= cap && lvl + 1 < P.n_levels) {
+        const int e = demote(P);
+        if (e != kErrNone) {
+          err = e;
+          return kFail;
+        }
+      }
+    }
+    const LevelDesc& L = P.lv[kMulti ? lvl : 0];
     int lo;
     double frac;
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
@@ -835,6 +881,7 @@ struct Fp64Lean {
     for (int a = 0; a < 3; ++a)
       if (a == axis) tn[a] += td;
     ++steps_;
+    if (kMulti) ++sal_;
 
     if (inside) {
       rp->w = left;
@@ -909,8 +956,8 @@ struct Fp64Lean {
     return q + P.qe * tau * div_rcp(last_ib2 - ib1, ib1, rib1) * pref;
   }
   __device__ __forceinline__ bool finite_state() const { return isfinite(tau); }
-  __device__ __forceinline__ int level() const { return 0; }
-  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int level() const { return kMulti ? lvl : 0; }
+  __device__ __forceinline__ int sal() const { return kMulti ? sal_ : steps_; }
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
@@ -964,6 +1011,13 @@ template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
   pool_kernel_body<Fp64Lean<kHint, kBrick, kPos>, false>(P);
+}
+
+// Multigrid variant of the lean tracer (n_levels > 1).
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+    trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
+  pool_kernel_body<Fp64Lean<0, false, true, true>, true>(P);
 }
 
 // Copies the fp64 k-fastest field into the 2x2x2 micro-brick layout.
@@ -1181,7 +1235,7 @@ namespace {
 // Kernel variant by (path, min blocks per SM); 4 or 5 blocks of 128 threads.
 using TraceFn = void (*)(TraceParams);
 bool lean_path(const TraceParams& P) {
-  return P.n_levels == 1 && P.n_temps >= 2 && P.lean &&
+  return P.n_temps >= 2 && P.lean &&
          P.lv[0].n[0] * static_cast<int64_t>(P.lv[0].n[1]) * P.lv[0].n[2] < (1LL << 31);
 }
 size_t fp64_smem(const TraceParams& P) {
@@ -1189,6 +1243,8 @@ size_t fp64_smem(const TraceParams& P) {
 }
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
+  if (P.n_levels > 1)
+    return min_blocks >= 6 ? trace_pool_fp64_lean_mg<6> : trace_pool_fp64_lean_mg<5>;
   if (!P.track_pos && !P.brick && P.cache_hint == 0)
     return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, false, false>
            : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, false, false>

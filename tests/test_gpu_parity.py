@@ -167,6 +167,8 @@ def test_device_rng_is_the_reference_stream():
     ("nb-3dimens", 10, dict(specular_walls=1)),  # all walls, specular
     ("box-sin-5", 9, {}),
     ("nb-parab", 12, dict(volume_sampling=1)),
+    ("nb-3dimens", 12, dict(n_levels=3, steps_per_level=3)),  # lean multigrid tracers
+    ("epsw-low", 10, dict(n_levels=2, steps_per_level=4)),
 ])
 def test_fp32_tracks_fp64_on_the_same_rays(name, n, variant):
     # Same seed: the fp32 kernel traces the reference's rays (same draws,

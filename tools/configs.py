@@ -180,13 +180,19 @@ def main():
                    time_slope=float(np.polyfit(lr, np.log([x[3] for x in rows]), 1)[0]))
     if "mg" in which:
         g, t, b, m, _ = W.channel_case(256, "nongrey16")
-        for lv in (1, 2, 3, 4):
-            cfg = capi.config_struct(rays_per_cell=64, seed=2024, n_levels=lv,
-                                     steps_per_level=5, coarsen_ratio=2)
-            q, sd, steps, ms, tms = device_solve(g, t, b, m, cfg)
-            record(a.out, **base(f"mg multigrid 256^3 levels={lv}", g, cfg, steps, ms, tms,
-                                 "fp64"),
-                   steps_per_level=[int(x) for x in steps], sigma_max=float(np.max(sd)))
+        for prec in ("fp64", "fp32"):
+            for lv in (1, 2, 3, 4):
+                cfg = capi.config_struct(rays_per_cell=64, seed=2024, n_levels=lv,
+                                         steps_per_level=5, coarsen_ratio=2,
+                                         precision=capi.FP64 if prec == "fp64" else capi.FP32)
+                q, sd, steps, ms, tms = device_solve(g, t, b, m, cfg)
+                rep = {}
+                if prec == "fp64" and lv > 1:
+                    rep["cpu_parity"] = cpu_check(g, t, b, m, cfg, q, sd, a.cells // 4)
+                record(a.out, **base(f"mg multigrid 256^3 levels={lv}", g, cfg, steps, ms, tms,
+                                     prec),
+                       steps_per_level=[int(x) for x in steps], sigma_max=float(np.max(sd)),
+                       sigma_median=float(np.median(sd)), **rep)
 
 
 if __name__ == "__main__":
