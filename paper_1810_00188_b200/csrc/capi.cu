@@ -285,6 +285,7 @@ struct Tune {
   int brick64 = 0;  // fp64: micro-brick field copy (measured neutral; off saves 8 B/cell)
   int sort = 1;  // narrow-band sorted dispatch (dispatch.cu)
   int track_pos = 0;  // 1 forces the position-tracking fp64 kernel
+  int tint_arith = 1;  // compute exact-uniform temperature records (fp64)
   int sort_tile_items = 1 << 16;
 };
 int env_int(const char* name, int fallback) {
@@ -305,6 +306,7 @@ const Tune& tune() {
     x.brick64 = env_int("ERMC_BRICK64", x.brick64);
     x.sort = env_int("ERMC_SORT", x.sort);
     x.track_pos = env_int("ERMC_TRACK_POS", x.track_pos);
+    x.tint_arith = env_int("ERMC_TINT_ARITH", x.tint_arith);
     x.sort_tile_items = std::max(1, env_int("ERMC_SORT_TILE", x.sort_tile_items));
     return x;
   }();
@@ -668,6 +670,16 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;
   P.inv_dt = 1.0 / v.dt;
+  // tint[l] = {temps[l], temps[l+1] - temps[l], RN(1/width)}: when every node
+  // is exactly l*dt + t0 (the kernel's expression, same two roundings) and
+  // every width exactly dt, the record is computed in the kernel instead of
+  // gathered (make_temp_grid's integer grids qualify).
+  P.inv_w = 1.0 / v.dt;
+  P.tint_arith = v.uniform && v.nt >= 2 && tune().tint_arith;
+  for (int l = 0; P.tint_arith && l + 1 < v.nt; ++l) {
+    const volatile double node = static_cast<double>(l) * v.dt;
+    if (node + v.t0 != v.temps[l] || v.temps[l + 1] - v.temps[l] != v.dt) P.tint_arith = 0;
+  }
   P.t_first = v.temps[0];
   P.t_last = v.temps[v.nt - 1];
   P.steps_per_level = s->d_steps.p;

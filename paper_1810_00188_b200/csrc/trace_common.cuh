@@ -62,6 +62,9 @@ struct TraceParams {
   const double4* tint;       // [n_temps-1] {t_lo, t_hi - t_lo, 1/(t_hi - t_lo), 0}
   const double4* iv64;       // [n_bands*n_quad][n_temps-1] {k_lo, k_hi, ib_lo, ib_hi}
   double inv_dt;             // 1/dt for the table-index estimate
+  double inv_w;              // RN(1 / dt): tint's reciprocal when tint_arith
+  int32_t tint_arith;        // every node is exactly l*dt + t0 and every width
+                             // exactly dt, so tint[l] is computed, not loaded
   double t_first, t_last;    // table range
 
   // ---- fp32 fast-path tables (trace_fp32.cu) ----

@@ -551,22 +551,33 @@ struct Fp32Lean {
 //            {inf, INT_MAX, 0, fixed index}                 (non-moving axis).
 // With even n a step leaves its brick exactly when the cells-left counter is
 // even before the step, for either direction.
-template <int kHint>
+// kPreV: the interval record of the next cell is loaded at the end of the
+// step that finds its temperature (one step ahead of its use) instead of at
+// the start of the step that uses it.
+template <int kHint, bool kPreV = false>
 struct Fp32Brick {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
+  float4 v_cur;  // kPreV: record of the current cell
+  float f_cur;   // kPreV: its interpolation weight
   double cq;
   const float4* row;
-  int4* ax;
+  // Per-axis records in two shared arrays so no access conflicts on banks:
+  //   axr[a] = {t_delta bits, cross-brick delta "far"}  (8 B: one LDS.64)
+  //            {inf, fixed index}                        (non-moving axis)
+  //   axl[a] = cells left before the face               (4 B, read + written)
+  // The in-brick delta is +-(4 >> a) with far's sign.
+  int2* axr;
+  int* axl;
   int lin, band, steps_;
   uint32_t next_draw, ray_id;
   uint64_t h_cell;
   int err;
 
   __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
-    const int4 r = ax[a * kBlock32];
-    if (r.z == 0) return r.w;
-    return r.z > 0 ? L.n[a] - 1 - r.y : r.y;
+    if (dir[a] == 0.0f) return axr[a * kBlock32].y;
+    const int left = axl[a * kBlock32];
+    return dir[a] > 0.0f ? L.n[a] - 1 - left : left;
   }
 
   __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx) {
@@ -578,7 +589,8 @@ struct Fp32Brick {
       const float da = dir[a];
       if (da == 0.0f) {
         tn[a] = __int_as_float(0x7f800000);
-        ax[a * kBlock32] = make_int4(0x7f800000, 0x7fffffff, 0, idx[a]);
+        axr[a * kBlock32] = make_int2(0x7f800000, idx[a]);
+        axl[a * kBlock32] = 0x7fffffff;
         continue;
       }
       const float inv = 1.0f / da;
@@ -587,10 +599,9 @@ struct Fp32Brick {
           static_cast<float>(L.origin[a] + (idx[a] + (up ? 1 : 0)) * L.d[a]);
       tn[a] = (face - p0[a]) * inv;
       const float td = static_cast<float>(L.d[a]) * fabsf(inv);
-      const int near = up ? sn[a] : -sn[a];
       const int far = up ? 8 * bs[a] - sn[a] : sn[a] - 8 * bs[a];
-      ax[a * kBlock32] =
-          make_int4(__float_as_int(td), up ? L.n[a] - 1 - idx[a] : idx[a], near, far);
+      axr[a * kBlock32] = make_int2(__float_as_int(td), far);
+      axl[a * kBlock32] = up ? L.n[a] - 1 - idx[a] : idx[a];
     }
     s = 0.0f;
     lin = brick_index(L, idx[0], idx[1], idx[2]);
@@ -608,7 +619,8 @@ struct Fp32Brick {
   __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
                                       uint32_t ray) {
     extern __shared__ int4 s_dyn[];
-    ax = s_dyn + threadIdx.x;
+    axr = reinterpret_cast<int2*>(s_dyn) + threadIdx.x;
+    axl = reinterpret_cast<int*>(reinterpret_cast<int2*>(s_dyn) + 3 * kBlock32) + threadIdx.x;
     Fp32Tracer base;
     const int e = base.init(P, cell, ray);
     if (e != kErrNone) return e;
@@ -629,18 +641,33 @@ struct Fp32Brick {
     ray_id = ray;
     h_cell = base.h_cell;
     t_cur = base.t_cur;  // the same value as the brick copy's
+    if (kPreV) lookup(P, t_cur);
     setup(P.lv[0], base.idx);
     return kErrNone;
+  }
+
+  __device__ __forceinline__ void lookup(const TraceParams& P, float t) {
+    const float u = fmaf(t, P.inv_dt32, P.u0_32);
+    const int lo = min(static_cast<int>(u), P.n_temps - 2);
+    f_cur = u - static_cast<float>(lo);
+    v_cur = ld_rec32<kHint>(row + lo);
   }
 
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
     if (tau <= P.tol32) return kDone;
     if (steps_ >= max_steps) return kDone;
     const LevelDesc& L = P.lv[0];
-    const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
-    const int lo = min(static_cast<int>(u), P.n_temps - 2);
-    const float f = u - static_cast<float>(lo);
-    const float4 v = ld_rec32<kHint>(row + lo);
+    float f;
+    float4 v;
+    if (kPreV) {
+      f = f_cur;
+      v = v_cur;
+    } else {
+      const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
+      const int lo = min(static_cast<int>(u), P.n_temps - 2);
+      f = u - static_cast<float>(lo);
+      v = ld_rec32<kHint>(row + lo);
+    }
 
     int axis = 0;
     float tmin = tn[0];
@@ -655,16 +682,18 @@ struct Fp32Brick {
     const float ds = fmaxf(tmin - s, 0.0f);
     s = fmaxf(tmin, s);
 
-    int4* rp = ax + axis * kBlock32;
-    const int4 r = *rp;
+    const int2 r = axr[axis * kBlock32];
+    int* lp = axl + axis * kBlock32;
+    const int left0 = *lp;
     const float td = __int_as_float(r.x);
+    const int far = r.y;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
       if (a == axis) tn[a] += td;
-    const int left = r.y - 1;
+    const int left = left0 - 1;
     const bool inside = left >= 0;
     const bool periodic = (P.periodic_mask >> axis) & 1;
-    int nlin = lin + ((r.y & 1) ? r.z : r.w);
+    int nlin = lin + ((left0 & 1) ? (far > 0 ? (4 >> axis) : -(4 >> axis)) : far);
     float t_next = t_cur;
     if (inside) {
       t_next = ld_t32<kHint>(L.field32b + nlin);
@@ -672,7 +701,7 @@ struct Fp32Brick {
       int idx[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        idx[a] = a == axis ? (r.z > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
+        idx[a] = a == axis ? (far > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
       nlin = brick_index(L, idx[0], idx[1], idx[2]);
       t_next = ld_t32<kHint>(L.field32b + nlin);
     }
@@ -687,24 +716,26 @@ struct Fp32Brick {
     ++steps_;
 
     if (inside) {
-      rp->y = left;
+      *lp = left;
       lin = nlin;
       t_cur = t_next;
+      if (kPreV) lookup(P, t_next);
       return kContinue;
     }
     if (periodic) {
-      rp->y = L.n[axis] - 1;
+      *lp = L.n[axis] - 1;
       rebase();
       const float ext = static_cast<float>(L.extent[axis]);
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        if (a == axis) p0[a] += r.z > 0 ? -ext : ext;
+        if (a == axis) p0[a] += far > 0 ? -ext : ext;
       lin = nlin;
       t_cur = t_next;
+      if (kPreV) lookup(P, t_next);
       return kContinue;
     }
     // wall exchange (tracer.cpp:155-165); the ray stays in its cell
-    const bool at_hi = r.z > 0;
+    const bool at_hi = far > 0;
     const int face = 2 * axis + (at_hi ? 1 : 0);
     const float ew = static_cast<float>(P.wall_eps[face]);
     const float ibw = __ldg(P.wall_ibn32 + face * P.n_bands + band);
@@ -761,10 +792,10 @@ struct Fp32Brick {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-template <int kMinBlocks, int kHint>
+template <int kMinBlocks, int kHint, bool kPreV = false>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp32Brick<kHint>, false>(P);
+  pool_kernel_body<Fp32Brick<kHint, kPreV>, false>(P);
 }
 
 // Converts the fp64 k-fastest field to the fp32 micro-brick layout.
@@ -851,6 +882,9 @@ TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   if (fp32_lean(P) && P.n_levels > 1)
     return min_blocks >= 8 ? trace_pool_fp32_lean_mg<8> : trace_pool_fp32_lean_mg<6>;
   if (fp32_lean(P) && P.brick) {
+    if (P.cache_hint == 3)  // experiment: record prefetched one step ahead
+      return min_blocks >= 8 ? trace_pool_fp32_brick<8, 0, true>
+                             : trace_pool_fp32_brick<6, 0, true>;
     if (P.cache_hint == 1) return trace_pool_fp32_brick<6, 1>;
     if (P.cache_hint == 2) return trace_pool_fp32_brick<6, 2>;
     return min_blocks >= 8 ? trace_pool_fp32_brick<8, 0> : trace_pool_fp32_brick<6, 0>;

@@ -422,8 +422,12 @@ __device__ __forceinline__ bool fast_lookup(const TraceParams& P,
     else
       l = static_cast<int>(x);
     l = min(max(l, 0), nt - 2);
-    double4 ti = ld_rec64<kHint>(P.tint + l);
     rec = ld_rec64<kHint>(row + l);
+    double4 ti;
+    if (P.tint_arith)  // the nodes are exactly t0 + l*dt (checked on the host)
+      ti = make_double4(static_cast<double>(l) * P.dt + P.t0, P.dt, P.inv_w, 0.0);
+    else
+      ti = ld_rec64<kHint>(P.tint + l);
     double f = div_rcp(T - ti.x, ti.y, ti.z);
     if ((f < 0.0 && l > 0) || (f > 1.0 && l < nt - 2)) {
       // rounding put T in the neighbouring interval (spectral.cpp:159-168)

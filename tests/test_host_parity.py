@@ -173,6 +173,16 @@ def test_solve_without_gpu_fails_loudly():
     g, t, b, m, _ = W.channel_case(4, "grey")
     with pytest.raises(capi.ErmcError, match="no CUDA device"):
         capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=2))
+    with pytest.raises(capi.ErmcError, match="no CUDA device"):
+        capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=2, n_devices=4))
+
+
+def test_n_devices_validation():
+    g, t, b, m, _ = W.channel_case(4, "grey")
+    with pytest.raises(capi.ErmcError, match="n_devices must be >= 0"):
+        capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=2, n_devices=-1))
+    c = E.SolveConfig()
+    assert c.n_devices == 1
 
 
 def test_channel_field_matches_survey_range():
