@@ -551,15 +551,10 @@ struct Fp32Lean {
 //            {inf, INT_MAX, 0, fixed index}                 (non-moving axis).
 // With even n a step leaves its brick exactly when the cells-left counter is
 // even before the step, for either direction.
-// kPreV: the interval record of the next cell is loaded at the end of the
-// step that finds its temperature (one step ahead of its use) instead of at
-// the start of the step that uses it.
-template <int kHint, bool kPreV = false>
+template <int kHint>
 struct Fp32Brick {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
-  float4 v_cur;  // kPreV: record of the current cell
-  float f_cur;   // kPreV: its interpolation weight
   double cq;
   const float4* row;
   // Per-axis records in two shared arrays so no access conflicts on banks:
@@ -641,33 +636,18 @@ struct Fp32Brick {
     ray_id = ray;
     h_cell = base.h_cell;
     t_cur = base.t_cur;  // the same value as the brick copy's
-    if (kPreV) lookup(P, t_cur);
     setup(P.lv[0], base.idx);
     return kErrNone;
-  }
-
-  __device__ __forceinline__ void lookup(const TraceParams& P, float t) {
-    const float u = fmaf(t, P.inv_dt32, P.u0_32);
-    const int lo = min(static_cast<int>(u), P.n_temps - 2);
-    f_cur = u - static_cast<float>(lo);
-    v_cur = ld_rec32<kHint>(row + lo);
   }
 
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
     if (tau <= P.tol32) return kDone;
     if (steps_ >= max_steps) return kDone;
     const LevelDesc& L = P.lv[0];
-    float f;
-    float4 v;
-    if (kPreV) {
-      f = f_cur;
-      v = v_cur;
-    } else {
-      const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
-      const int lo = min(static_cast<int>(u), P.n_temps - 2);
-      f = u - static_cast<float>(lo);
-      v = ld_rec32<kHint>(row + lo);
-    }
+    const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
+    const int lo = min(static_cast<int>(u), P.n_temps - 2);
+    const float f = u - static_cast<float>(lo);
+    const float4 v = ld_rec32<kHint>(row + lo);
 
     int axis = 0;
     float tmin = tn[0];
@@ -719,7 +699,6 @@ struct Fp32Brick {
       *lp = left;
       lin = nlin;
       t_cur = t_next;
-      if (kPreV) lookup(P, t_next);
       return kContinue;
     }
     if (periodic) {
@@ -731,7 +710,6 @@ struct Fp32Brick {
         if (a == axis) p0[a] += far > 0 ? -ext : ext;
       lin = nlin;
       t_cur = t_next;
-      if (kPreV) lookup(P, t_next);
       return kContinue;
     }
     // wall exchange (tracer.cpp:155-165); the ray stays in its cell
@@ -792,10 +770,10 @@ struct Fp32Brick {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-template <int kMinBlocks, int kHint, bool kPreV = false>
+template <int kMinBlocks, int kHint>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp32Brick<kHint, kPreV>, false>(P);
+  pool_kernel_body<Fp32Brick<kHint>, false>(P);
 }
 
 // Converts the fp64 k-fastest field to the fp32 micro-brick layout.
@@ -882,9 +860,6 @@ TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   if (fp32_lean(P) && P.n_levels > 1)
     return min_blocks >= 8 ? trace_pool_fp32_lean_mg<8> : trace_pool_fp32_lean_mg<6>;
   if (fp32_lean(P) && P.brick) {
-    if (P.cache_hint == 3)  // experiment: record prefetched one step ahead
-      return min_blocks >= 8 ? trace_pool_fp32_brick<8, 0, true>
-                             : trace_pool_fp32_brick<6, 0, true>;
     if (P.cache_hint == 1) return trace_pool_fp32_brick<6, 1>;
     if (P.cache_hint == 2) return trace_pool_fp32_brick<6, 2>;
     return min_blocks >= 8 ? trace_pool_fp32_brick<8, 0> : trace_pool_fp32_brick<6, 0>;
