@@ -225,10 +225,20 @@ def run_b200(a, world, rank, local):
 
     from paper_1810_00188_b200 import capi, parallel, workloads as W
 
+    # ERMC_BENCH_BACKEND=gloo (test only): ranks may share one GPU (device =
+    # local rank mod visible devices) and the collectives go through host
+    # memory, so the N > 1 flow can be exercised on a one-GPU box. Timings
+    # from such a run mean nothing; the driver's runs use NCCL, one GPU each.
+    backend = os.environ.get("ERMC_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # collective tensors
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
@@ -245,14 +255,14 @@ def run_b200(a, world, rank, local):
     def max_over_ranks(x):
         if world == 1:
             return x
-        v = torch.tensor([x], dtype=torch.float64, device=dev)
+        v = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         return float(v.item())
 
     def sum_over_ranks(x):
         if world == 1:
             return x
-        v = torch.tensor([x], dtype=torch.int64, device=dev)
+        v = torch.tensor([x], dtype=torch.int64, device=cdev)
         dist.all_reduce(v, op=dist.ReduceOp.SUM)
         return int(v.item())
 
@@ -389,7 +399,7 @@ def run_b200(a, world, rank, local):
                     "generated through the solver API)",
             "config": {"workload": workload_name(a), "grid": a.grid, "rays_per_cell": a.rays,
                        "model": a.model, "precision": a.precision,
-                       "parallelism": f"x-slabs x{world}" + (" + NCCL all-gather" if world > 1
+                       "parallelism": f"x-slabs x{world}" + (f" + {backend} all-gather" if world > 1
                                                              else ""),
                        "l2": "flushed (256 MiB write) before every step"},
             "s_per_field": el_max * 1e-3 / a.steps,

@@ -339,7 +339,6 @@ struct ermc_session {
   DevBuf<double> d_field64b;
   std::vector<std::unique_ptr<DevBuf<float>>> d_levels32;
   DevBuf<float4> d_iv32;
-  cudaTextureObject_t tex_t32b = 0, tex_iv32 = 0;  // TEX-pipe experiments
   bool iv32_ready = false;
   DevBuf<double> d_qray;
   // narrow-band sorted dispatch: row rank by k(n,g,T_max), keys, order
@@ -361,8 +360,6 @@ struct ermc_session {
   // wait for it before the buffers return to the pool.
   cudaEvent_t last_work = nullptr;
   ~ermc_session() {
-    if (tex_t32b) cudaDestroyTextureObject(tex_t32b);
-    if (tex_iv32) cudaDestroyTextureObject(tex_iv32);
     if (last_work) {
       DeviceGuard g(device);
       cudaEventSynchronize(last_work);
@@ -921,10 +918,6 @@ void set_field_impl(ermc_session* s, const double* t, int is_device,
   s->d_field32.reset();
   s->d_field32b.reset();
   s->d_field64b.reset();
-  if (s->tex_t32b) {
-    cudaDestroyTextureObject(s->tex_t32b);
-    s->tex_t32b = 0;
-  }
 }
 
 void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
@@ -964,29 +957,7 @@ void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
       ++s->launches;
     }
     P.lv[0].field32b = s->d_field32b.p;
-    if (tune().cache_hint >= 4) {  // texture objects for the TEX-pipe variants
-      auto make_tex = [](void* ptr, size_t bytes, cudaChannelFormatDesc desc) {
-        cudaResourceDesc rd{};
-        rd.resType = cudaResourceTypeLinear;
-        rd.res.linear.devPtr = ptr;
-        rd.res.linear.desc = desc;
-        rd.res.linear.sizeInBytes = bytes;
-        cudaTextureDesc td{};
-        td.readMode = cudaReadModeElementType;
-        cudaTextureObject_t t = 0;
-        cuda_check(cudaCreateTextureObject(&t, &rd, &td, nullptr), "cudaCreateTextureObject");
-        return t;
-      };
-      if (!s->tex_t32b)
-        s->tex_t32b = make_tex(s->d_field32b.p, s->n_cells * sizeof(float),
-                               cudaCreateChannelDesc<float>());
-      if (!s->tex_iv32)
-        s->tex_iv32 = make_tex(s->d_iv32.p, s->d_iv32.n * sizeof(float4),
-                               cudaCreateChannelDesc<float4>());
-    }
   }
-  P.tex_t32b = s->tex_t32b;
-  P.tex_iv32 = s->tex_iv32;
   s->d_levels32.resize(s->config.n_levels);
   for (int l = 1; l < s->config.n_levels; ++l) {
     const int64_t n = cells_of(s->level_grids[l]);

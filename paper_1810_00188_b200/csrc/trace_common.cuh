@@ -70,9 +70,6 @@ struct TraceParams {
   // ---- fp32 fast-path tables (trace_fp32.cu) ----
   const float4* iv32;        // [n_bands*n_quad][n_temps-1] {k_lo, k_hi-k_lo, ib_lo, ib_hi-ib_lo}
   const float* wall_ibn32;   // [6][n_bands] wall Ib / Ib(n, T_last)
-  // Texture objects over field32b / iv32 (fetches on the TEX pipe instead of
-  // the LSU pipe; 0 = not created). cudaTextureObject_t is 64-bit.
-  unsigned long long tex_t32b, tex_iv32;
   float inv_dt32;            // 1/dt for the fp32 lookup (uniform grids only)
   float t0_32;
   float tol32;               // tolerance as float

@@ -647,8 +647,7 @@ struct Fp32Brick {
     const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
     const int lo = min(static_cast<int>(u), P.n_temps - 2);
     const float f = u - static_cast<float>(lo);
-    const float4 v = kHint >= 5 ? tex1Dfetch<float4>(P.tex_iv32, static_cast<int>(row - P.iv32) + lo)
-                                 : ld_rec32<(kHint >= 4 ? 0 : kHint)>(row + lo);
+    const float4 v = ld_rec32<kHint>(row + lo);
 
     int axis = 0;
     float tmin = tn[0];
@@ -677,16 +676,14 @@ struct Fp32Brick {
     int nlin = lin + ((left0 & 1) ? (far > 0 ? (4 >> axis) : -(4 >> axis)) : far);
     float t_next = t_cur;
     if (inside) {
-      t_next = (kHint == 4 || kHint == 6 ? tex1Dfetch<float>(P.tex_t32b, nlin)
-                                              : ld_t32<(kHint >= 4 ? 0 : kHint)>(L.field32b + nlin));
+      t_next = ld_t32<kHint>(L.field32b + nlin);
     } else if (periodic) {
       int idx[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
         idx[a] = a == axis ? (far > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
       nlin = brick_index(L, idx[0], idx[1], idx[2]);
-      t_next = (kHint == 4 || kHint == 6 ? tex1Dfetch<float>(P.tex_t32b, nlin)
-                                              : ld_t32<(kHint >= 4 ? 0 : kHint)>(L.field32b + nlin));
+      t_next = ld_t32<kHint>(L.field32b + nlin);
     }
 
     const float kappa = fmaf(f, v.y, v.x);
@@ -863,10 +860,6 @@ TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   if (fp32_lean(P) && P.n_levels > 1)
     return min_blocks >= 8 ? trace_pool_fp32_lean_mg<8> : trace_pool_fp32_lean_mg<6>;
   if (fp32_lean(P) && P.brick) {
-    // texture-pipe experiments: 4 = T via TEX, 5 = records via TEX, 6 = both
-    if (P.cache_hint == 4 && P.tex_t32b) return trace_pool_fp32_brick<8, 4>;
-    if (P.cache_hint == 5 && P.tex_iv32) return trace_pool_fp32_brick<8, 5>;
-    if (P.cache_hint == 6 && P.tex_t32b && P.tex_iv32) return trace_pool_fp32_brick<8, 6>;
     if (P.cache_hint == 1) return trace_pool_fp32_brick<6, 1>;
     if (P.cache_hint == 2) return trace_pool_fp32_brick<6, 2>;
     return min_blocks >= 8 ? trace_pool_fp32_brick<8, 0> : trace_pool_fp32_brick<6, 0>;

@@ -55,12 +55,16 @@ def gather_slabs(local, slabs: list[Slab], dist, group=None):
     import torch  # noqa: PLC0415
 
     width = max(s.n for s in slabs)
-    buf = local.new_zeros(width)
-    buf[: local.numel()] = local
-    out = local.new_zeros(width * len(slabs))
+    # NCCL gathers device tensors in place; gloo (CPU tests) through the host.
+    staged = local.is_cuda and dist.get_backend(group) != "nccl"
+    src = local.cpu() if staged else local
+    buf = src.new_zeros(width)
+    buf[: src.numel()] = src
+    out = src.new_zeros(width * len(slabs))
     dist.all_gather_into_tensor(out, buf, group=group)
     parts = [out[r * width: r * width + s.n] for r, s in enumerate(slabs)]
-    return torch.cat(parts)
+    full = torch.cat(parts)
+    return full.to(local.device) if staged else full
 
 
 def sum_counters(steps, dist, group=None):
