@@ -551,7 +551,10 @@ struct Fp32Lean {
 //            {inf, INT_MAX, 0, fixed index}                 (non-moving axis).
 // With even n a step leaves its brick exactly when the cells-left counter is
 // even before the step, for either direction.
-template <int kHint>
+// kPos = false when every wall is black: a wall hit ends the ray, so the
+// position (p0) and direction are dead after setup and periodic re-basing
+// only shifts the ray parameter (frees 6 registers; see Fp64Lean).
+template <int kHint, bool kPos = true>
 struct Fp32Brick {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
@@ -605,7 +608,7 @@ struct Fp32Brick {
   __device__ __forceinline__ void rebase() {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      p0[a] = fmaf(s, dir[a], p0[a]);
+      if (kPos) p0[a] = fmaf(s, dir[a], p0[a]);
       tn[a] -= s;
     }
     s = 0.0f;
@@ -707,7 +710,7 @@ struct Fp32Brick {
       const float ext = static_cast<float>(L.extent[axis]);
 #pragma unroll
       for (int a = 0; a < 3; ++a)
-        if (a == axis) p0[a] += far > 0 ? -ext : ext;
+        if (kPos && a == axis) p0[a] += far > 0 ? -ext : ext;
       lin = nlin;
       t_cur = t_next;
       return kContinue;
@@ -721,6 +724,7 @@ struct Fp32Brick {
     acc = fmaf(tw, ibw - ib1n, acc);
     tau -= tw;
     if (tau <= P.tol32) return kDone;
+    if (!kPos) return kDone;  // black walls: tau is 0 here unless non-finite
     // reflection (tracer.cpp:167-182)
     int idx[3];
 #pragma unroll
@@ -770,10 +774,10 @@ struct Fp32Brick {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-template <int kMinBlocks, int kHint>
+template <int kMinBlocks, int kHint, bool kPos = true>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
-  pool_kernel_body<Fp32Brick<kHint>, false>(P);
+  pool_kernel_body<Fp32Brick<kHint, kPos>, false>(P);
 }
 
 // Converts the fp64 k-fastest field to the fp32 micro-brick layout.
@@ -862,6 +866,11 @@ TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   if (fp32_lean(P) && P.brick) {
     if (P.cache_hint == 1) return trace_pool_fp32_brick<6, 1>;
     if (P.cache_hint == 2) return trace_pool_fp32_brick<6, 2>;
+    if (!P.track_pos)
+      return min_blocks >= 12  ? trace_pool_fp32_brick<12, 0, false>
+             : min_blocks >= 10 ? trace_pool_fp32_brick<10, 0, false>
+             : min_blocks >= 8 ? trace_pool_fp32_brick<8, 0, false>
+                               : trace_pool_fp32_brick<6, 0, false>;
     return min_blocks >= 8 ? trace_pool_fp32_brick<8, 0> : trace_pool_fp32_brick<6, 0>;
   }
   if (fp32_lean(P))

@@ -913,6 +913,11 @@ struct Fp64Lean {
     q += P.qe * tau * ew * div_rcp(ib_w - ib1, ib1, rib1) * pref;
     tau *= 1.0 - ew;
     if (tau <= P.tol) return kDone;
+    // !kPos: every wall is black, so tau is 0 here unless it is not finite;
+    // ending the ray then leaves the report to the pool's finite-state check,
+    // and with no reflection code the position and direction are dead after
+    // setup (12 registers).
+    if (!kPos) return kDone;
     int idx[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);
@@ -1245,12 +1250,24 @@ bool lean_path(const TraceParams& P) {
 size_t fp64_smem(const TraceParams& P) {
   return lean_path(P) ? kLeanRecs64 * kBlock * sizeof(int4) : 0;
 }
+// min_blocks = 0 picks the measured best per variant (B200, 256^3 channel):
+// 8 blocks/SM for the black-wall tracer (64 registers + 128 B of L1-resident
+// spills beat 6 blocks / 80 registers by 12 %; 9+ blocks lose again),
+// 6 for the position-tracking and multigrid tracers (80 registers).
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
+  const bool black = !P.track_pos && !P.brick && P.cache_hint == 0 && P.n_levels == 1;
+  if (min_blocks <= 0) min_blocks = black ? 8 : 6;
   if (P.n_levels > 1)
-    return min_blocks >= 6 ? trace_pool_fp64_lean_mg<6> : trace_pool_fp64_lean_mg<5>;
-  if (!P.track_pos && !P.brick && P.cache_hint == 0)
-    return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, false, false>
+    return min_blocks >= 7   ? trace_pool_fp64_lean_mg<7>
+           : min_blocks == 6 ? trace_pool_fp64_lean_mg<6>
+                             : trace_pool_fp64_lean_mg<5>;
+  if (black)
+    return min_blocks >= 12  ? trace_pool_fp64_lean<12, 0, false, false>
+           : min_blocks >= 10 ? trace_pool_fp64_lean<10, 0, false, false>
+           : min_blocks == 9 ? trace_pool_fp64_lean<9, 0, false, false>
+           : min_blocks == 8 ? trace_pool_fp64_lean<8, 0, false, false>
+           : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, false>
            : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, false, false>
                              : trace_pool_fp64_lean<5, 0, false, false>;
   if (P.cache_hint == 1)
@@ -1268,6 +1285,7 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
                            : trace_pool_fp64_lean<5, 0, false>;
 }
 TraceFn fp64_kernel(bool multi, int min_blocks) {
+  if (min_blocks <= 0) min_blocks = 5;
   if (multi) return min_blocks >= 5 ? trace_pool_fp64<true, 5> : trace_pool_fp64<true, 4>;
   return min_blocks >= 5 ? trace_pool_fp64<false, 5> : trace_pool_fp64<false, 4>;
 }
