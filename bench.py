@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--model", default="nongrey16")
     p.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     p.add_argument("--seed", type=int, default=2024)
+    p.add_argument("--wall-eps", type=float, default=1.0,
+                   help="channel wall emissivity (1 = config 4's black walls)")
     p.add_argument("--no-fp32-extra", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -79,8 +81,9 @@ def peaks():
 
 
 def workload_name(a):
+    walls = "" if a.wall_eps == 1.0 else f", grey walls eps={a.wall_eps}"
     return (f"config4: {a.grid}^3 synthetic turbulent channel, {a.model} correlated-k "
-            f"(elsasser, 16 g), R={a.rays} rays/cell, seed {a.seed}")
+            f"(elsasser, 16 g), R={a.rays} rays/cell, seed {a.seed}{walls}")
 
 
 # ----------------------------------------------------------------- clocks
@@ -186,7 +189,7 @@ def run_reference(a, world, rank):
         return
     from paper_1810_00188_b200 import capi, workloads as W
 
-    grid, t, b, m, _ = W.channel_case(a.grid, a.model)
+    grid, t, b, m, _ = W.channel_case(a.grid, a.model, wall_eps=a.wall_eps)
     cfg = capi.config_struct(rays_per_cell=a.rays, seed=a.seed, workers=os.cpu_count() or 1)
     threads = os.cpu_count() or 1
     ref = CpuReference(grid, t, b, m, cfg, threads)
@@ -242,7 +245,7 @@ def run_b200(a, world, rank, local):
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
 
-    grid, t_host, b, m, _ = W.channel_case(a.grid, a.model)
+    grid, t_host, b, m, _ = W.channel_case(a.grid, a.model, wall_eps=a.wall_eps)
     n_cells = grid.nx * grid.ny * grid.nz
     slabs = parallel.all_slabs(grid.nx, grid.ny, grid.nz, world)
     slab = slabs[rank]

@@ -1253,11 +1253,12 @@ size_t fp64_smem(const TraceParams& P) {
 // min_blocks = 0 picks the measured best per variant (B200, 256^3 channel):
 // 8 blocks/SM for the black-wall tracer (64 registers + 128 B of L1-resident
 // spills beat 6 blocks / 80 registers by 12 %; 9+ blocks lose again),
-// 6 for the position-tracking and multigrid tracers (80 registers).
+// 7 for the position-tracking tracer (grey walls, 256^3 eps = 0.5: +7 % over
+// 6), 6 for the multigrid tracer (7 measured no better).
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
   const bool black = !P.track_pos && !P.brick && P.cache_hint == 0 && P.n_levels == 1;
-  if (min_blocks <= 0) min_blocks = black ? 8 : 6;
+  if (min_blocks <= 0) min_blocks = black ? 8 : P.n_levels > 1 ? 6 : 7;
   if (P.n_levels > 1)
     return min_blocks >= 7   ? trace_pool_fp64_lean_mg<7>
            : min_blocks == 6 ? trace_pool_fp64_lean_mg<6>
@@ -1280,7 +1281,8 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
     return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, true>
            : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, true>
                              : trace_pool_fp64_lean<5, 0, true>;
-  return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, false>
+  return min_blocks >= 8   ? trace_pool_fp64_lean<8, 0, false>
+         : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false>
          : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, false>
                            : trace_pool_fp64_lean<5, 0, false>;
 }

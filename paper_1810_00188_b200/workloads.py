@@ -62,10 +62,11 @@ def channel_field(n: int) -> np.ndarray:
     return np.ascontiguousarray(t.reshape(-1))
 
 
-def channel_boundary() -> capi.Boundary:
+def channel_boundary(wall_eps: float = 1.0) -> capi.Boundary:
+    """Paper channel walls (black by default; grey walls reflect diffusely)."""
     return capi.make_boundary((capi.PERIODIC, capi.WALL, capi.PERIODIC),
-                              [(0.0, 1.0), (T_WALL_LO, 1.0), (0.0, 1.0)],
-                              [(0.0, 1.0), (T_WALL_HI, 1.0), (0.0, 1.0)])
+                              [(0.0, 1.0), (T_WALL_LO, wall_eps), (0.0, 1.0)],
+                              [(0.0, 1.0), (T_WALL_HI, wall_eps), (0.0, 1.0)])
 
 
 def _ermc():
@@ -88,7 +89,7 @@ def nongrey_channel_model(n_bands: int = 16, n_quad: int = 16, strength: float =
                                   E.QuadratureSet.gauss_legendre(n_quad))
 
 
-def channel_case(n: int, model: str = "nongrey16", tau: float = 1.0):
+def channel_case(n: int, model: str = "nongrey16", tau: float = 1.0, wall_eps: float = 1.0):
     """(grid, T, boundary, ModelArrays, model_object) for a channel config."""
     if model.startswith("nongrey"):
         nb = int(model[len("nongrey"):] or 16)
@@ -97,4 +98,5 @@ def channel_case(n: int, model: str = "nongrey16", tau: float = 1.0):
         m = grey_channel_model(tau)
     else:
         raise ValueError(model)
-    return channel_grid(n), channel_field(n), channel_boundary(), capi.model_from_ermc(m), m
+    return (channel_grid(n), channel_field(n), channel_boundary(wall_eps),
+            capi.model_from_ermc(m), m)
