@@ -70,9 +70,10 @@ def build_lib(force: bool = False, verbose: bool = True) -> Path:
         return LIB
     OBJ.mkdir(exist_ok=True)
     jobs = []
+    exp_flags = os.environ.get("ERMC_NVCC_FLAGS", "").split()  # A/B experiments only
     for src, extra in CUDA_SOURCES:
         obj = OBJ / (src + ".o")
-        jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17",
+        jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *exp_flags,
                      "-Xcompiler", "-fPIC", "-Xptxas", "-v", *extra,
                      f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(CSRC / src),
                      "-o", str(obj)])

@@ -8,13 +8,16 @@ the GPU path through it. Descriptors can be built from numpy arrays or from
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 from typing import Sequence
 
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libermc_b200.so"
+LIB_PATH = Path(os.environ.get("ERMC_B200_LIB", _HERE / "libermc_b200.so"))
+# ERMC_B200_LIB: load another build of the same library (A/B experiments on
+# one GPU box; tools/ab_lib.sh).
 
 PERIODIC, WALL = 0, 1
 FP64, FP32 = 0, 1
