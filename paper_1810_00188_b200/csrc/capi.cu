@@ -280,7 +280,6 @@ struct Tune {
   int fp64_min_blocks = 0;  // 0 = per-tracer default (trace_fp64.cu)
   int fp32_min_blocks = 8;
   int lean = 1;
-  int cache_hint = 0;
   int brick = 1;    // fp32: micro-brick field copy (measured +4 %)
   int brick64 = 0;  // fp64: micro-brick field copy (measured neutral; off saves 8 B/cell)
   int sort = 1;  // narrow-band sorted dispatch (dispatch.cu)
@@ -301,7 +300,6 @@ const Tune& tune() {
     x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
     x.lean = env_int("ERMC_LEAN", x.lean);
-    x.cache_hint = env_int("ERMC_CACHE_HINT", x.cache_hint);
     x.brick = env_int("ERMC_BRICK", x.brick);
     x.brick64 = env_int("ERMC_BRICK64", x.brick64);
     x.sort = env_int("ERMC_SORT", x.sort);
@@ -665,7 +663,6 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.refill_threshold = tune().refill;
   P.inner_steps = tune().inner_steps;
   P.lean = tune().lean;
-  P.cache_hint = tune().cache_hint;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;

@@ -45,7 +45,9 @@ __device__ __forceinline__ double4 ldg4(const double4* p) {
   return r;
 }
 
-// Cache-hinted read-only loads for the march (kHint: 0 = plain LDG.CONSTANT,
+// Cache-hinted read-only loads for the march; the kernels instantiate
+// kHint = 0 (the hinted variants measured 5-27 % slower on B200, see
+// profiles/ROUND1.md) (kHint: 0 = plain LDG.CONSTANT,
 // 1 = temperature gathers bypass L1 allocation, 2 = temperature gathers evict
 // first; for kHint >= 1 the interval records are kept with evict_last).
 template <int kHint>

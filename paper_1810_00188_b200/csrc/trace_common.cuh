@@ -88,7 +88,6 @@ struct TraceParams {
   int32_t refill_threshold;  // idle lanes before a warp regenerates rays
   int32_t inner_steps;       // march steps between two pool checks
   int32_t lean;              // fp64: 1 = lean tracer (per-axis records in smem)
-  int32_t cache_hint;        // L1 policy of the lean tracers' loads (0, 1, 2)
   int32_t brick;             // lean tracers read the micro-brick field copy
   int32_t track_pos;         // 0 when every wall is black (positions never read)
   int64_t cell_base;         // first global linear cell of this chunk

@@ -1278,39 +1278,27 @@ size_t fp64_smem(const TraceParams& P) {
 }
 // min_blocks = 0 picks the measured best per variant (B200, 256^3 channel):
 // 8 blocks/SM for the black-wall tracer (64 registers + 128 B of L1-resident
-// spills beat 6 blocks / 80 registers by 12 %; 9+ blocks lose again),
+// spills in the refill path beat 6 blocks / 80 registers by 12 %; 9, 10, 12
+// blocks lose again: 0.98, 0.89, 0.77x of 8),
 // 7 for the position-tracking tracer (grey walls, 256^3 eps = 0.5: +7 % over
 // 6), 6 for the multigrid tracer (7 measured no better).
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
-  const bool black = !P.track_pos && !P.brick && P.cache_hint == 0 && P.n_levels == 1;
-  if (min_blocks <= 0) min_blocks = black ? 8 : P.n_levels > 1 ? 6 : 7;
+  const bool brick = P.brick && P.lv[0].field64b;
+  if (min_blocks <= 0) min_blocks = P.n_levels > 1 ? 6 : !P.track_pos ? 8 : 7;
+  min_blocks = min(max(min_blocks, 6), 8);
   if (P.n_levels > 1)
-    return min_blocks >= 7   ? trace_pool_fp64_lean_mg<7>
-           : min_blocks == 6 ? trace_pool_fp64_lean_mg<6>
-                             : trace_pool_fp64_lean_mg<5>;
-  if (black)
-    return min_blocks >= 12  ? trace_pool_fp64_lean<12, 0, false, false>
-           : min_blocks >= 10 ? trace_pool_fp64_lean<10, 0, false, false>
-           : min_blocks == 9 ? trace_pool_fp64_lean<9, 0, false, false>
-           : min_blocks == 8 ? trace_pool_fp64_lean<8, 0, false, false>
+    return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7> : trace_pool_fp64_lean_mg<6>;
+  if (!P.track_pos) {
+    if (brick) return trace_pool_fp64_lean<8, 0, true, false>;
+    return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, false>
            : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, false>
-           : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, false, false>
-                             : trace_pool_fp64_lean<5, 0, false, false>;
-  if (P.cache_hint == 1)
-    return P.brick && P.lv[0].field64b ? trace_pool_fp64_lean<6, 1, true>
-                                       : trace_pool_fp64_lean<6, 1, false>;
-  if (P.cache_hint == 2)
-    return P.brick && P.lv[0].field64b ? trace_pool_fp64_lean<6, 2, true>
-                                       : trace_pool_fp64_lean<6, 2, false>;
-  if (P.brick && P.lv[0].field64b)
-    return min_blocks >= 7   ? trace_pool_fp64_lean<7, 0, true>
-           : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, true>
-                             : trace_pool_fp64_lean<5, 0, true>;
-  return min_blocks >= 8   ? trace_pool_fp64_lean<8, 0, false>
+                             : trace_pool_fp64_lean<6, 0, false, false>;
+  }
+  if (brick) return trace_pool_fp64_lean<7, 0, true>;
+  return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false>
          : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false>
-         : min_blocks == 6 ? trace_pool_fp64_lean<6, 0, false>
-                           : trace_pool_fp64_lean<5, 0, false>;
+                           : trace_pool_fp64_lean<6, 0, false>;
 }
 TraceFn fp64_kernel(bool multi, int min_blocks) {
   if (min_blocks <= 0) min_blocks = 5;
