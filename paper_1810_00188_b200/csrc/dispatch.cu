@@ -62,7 +62,8 @@ __device__ __forceinline__ int upper_bound_any(const double* a, int n, double x)
 // band / g CDFs when they fit (cdf_len > 0).
 __global__ void __launch_bounds__(kSortBlock)
     ng_tile_sort(const __grid_constant__ TraceParams P, const int32_t* __restrict__ row_rank,
-                 int n_bins, int cdf_len, uint32_t tile_items, uint32_t* __restrict__ packed,
+                 int n_bins, int dir_bins, int cdf_len, uint32_t tile_items,
+                 uint32_t* __restrict__ packed,
                  uint32_t* __restrict__ perm) {
   extern __shared__ __align__(8) unsigned char s_raw[];
   double* s_cdf = reinterpret_cast<double*>(s_raw);
@@ -89,7 +90,17 @@ __global__ void __launch_bounds__(kSortBlock)
     if (bn >= nb) bn = nb - 1;
     int g = upper_bound_any(quad_cdf + bn * nq, nq, draw_u(h_cell, ray, 3));
     if (g >= nq) g = nq - 1;
-    const unsigned key = static_cast<unsigned>(__ldg(row_rank + bn * nq + g));
+    unsigned key = static_cast<unsigned>(__ldg(row_rank + bn * nq + g));
+    if (dir_bins > 1) {
+      // Direction bin from draws 0 and 1 (sampling.cpp:31-40): cos(theta) =
+      // 1 - 2 u0 and phi = 2 pi u1, binned uniformly in u0 and u1, so rays of
+      // one spectral row that travel alike sit in adjacent lanes.
+      const int nth = dir_bins >= 32 ? 4 : 2;
+      const int nph = dir_bins / nth;
+      const int bt = min(static_cast<int>(draw_u(h_cell, ray, 0) * nth), nth - 1);
+      const int bp = min(static_cast<int>(draw_u(h_cell, ray, 1) * nph), nph - 1);
+      key = key * dir_bins + bt * nph + bp;
+    }
     const unsigned rank = atomicAdd(&s_cur[key], 1u);
     packed[w] = key << 16 | rank;
   }
@@ -130,8 +141,11 @@ __global__ void __launch_bounds__(kSortBlock)
 int sort_max_bins() { return kMaxSortBins; }
 int sort_max_tile_items() { return 1 << 16; }
 
-cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_bins,
-                           int tile_cells, uint32_t* packed, uint32_t* perm, cudaStream_t s) {
+cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_rows,
+                           int dir_bins, int tile_cells, uint32_t* packed, uint32_t* perm,
+                           cudaStream_t s) {
+  while (dir_bins > 1 && n_rows * dir_bins > kMaxSortBins) dir_bins /= 2;
+  const int n_bins = n_rows * dir_bins;
   if (P.n_work == 0) return cudaSuccess;
   const uint32_t tile_items = static_cast<uint32_t>(tile_cells) * static_cast<uint32_t>(P.rays);
   if (n_bins > kMaxSortBins || tile_items > (1u << 16)) return cudaErrorInvalidValue;
@@ -145,7 +159,8 @@ cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_
   }
   const uint32_t n = static_cast<uint32_t>(P.n_work);
   const uint32_t tiles = (n + tile_items - 1) / tile_items;
-  ng_tile_sort<<<tiles, kSortBlock, smem, s>>>(P, row_rank, n_bins, cdf_len, tile_items,
+  ng_tile_sort<<<tiles, kSortBlock, smem, s>>>(P, row_rank, n_bins, dir_bins, cdf_len,
+                                               tile_items,
                                                packed, perm);
   return cudaGetLastError();
 }

@@ -239,3 +239,31 @@ def test_multi_device_split_is_byte_identical(n_devices):
     part = capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=32, seed=4,
                                                      n_devices=n_devices), cell_range=(lo, hi))
     assert np.array_equal(part[0], one[0][lo:hi])
+
+
+def test_edge_sizes_match_reference():
+    # Degenerate inputs the reference accepts: one ray per cell (std_dev = 0,
+    # solver.cpp:150-153), a one-cell grid, a one-cell-thick slab, an empty
+    # cell range, and a max_steps cap that truncates most rays.
+    grid, t, b, m, _ = refshim.ref_case("nb-parab", 6)
+    for cfg in (capi.config_struct(rays_per_cell=1, seed=21),
+                capi.config_struct(rays_per_cell=16, seed=22, max_steps=3)):
+        (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(grid, t, b, m, cfg)
+        assert total == rtotal and list(steps) == list(rsteps)
+        assert_fp64_parity(q, rq, sd, rsd)
+        if cfg.rays_per_cell == 1:
+            assert np.all(sd == 0.0)
+    q, sd, steps, total, _ = capi.solve(grid, t, b, m, capi.config_struct(rays_per_cell=8),
+                                        cell_range=(5, 5))
+    assert q.size == 0 and total == 0
+    for shape in ((1, 1, 1), (1, 5, 7), (9, 1, 1)):
+        g = capi.make_grid(shape, (0.1, 0.2, 0.3))
+        n = shape[0] * shape[1] * shape[2]
+        tt = np.linspace(600.0, 1000.0, n) if n > 1 else np.array([900.0])
+        bb = capi.make_boundary((capi.WALL, capi.PERIODIC, capi.WALL),
+                                [(500.0, 1.0), (0.0, 1.0), (800.0, 0.3)],
+                                [(1000.0, 0.5), (0.0, 1.0), (0.0, 1.0)])
+        cfg = capi.config_struct(rays_per_cell=40, seed=23)
+        (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(g, tt, bb, m, cfg)
+        assert total == rtotal, shape
+        assert_fp64_parity(q, rq, sd, rsd)
