@@ -7,8 +7,8 @@
 //
 // Not provided (out of the hot-path scope): the per-ray
 // sampling/tracer API (init_ray, march — they exist only inside the trace
-// kernel; tests drive them through ermc_b200_trace_rays), face_distances,
-// the verification cases and analytic oracles, and the CLI.
+// kernel; tests drive them through ermc_b200_trace_rays), the verification
+// cases and analytic oracles, and the CLI.
 #pragma once
 
 #include <array>
@@ -112,6 +112,17 @@ std::array<int, 3> locate(const CartesianGrid& grid, const Vec3& point,
                           const Vec3& dir);
 
 inline constexpr double kInf = std::numeric_limits<double>::infinity();
+
+// face_distances (reference geometry.hpp:100-109): distance to the next cell
+// face along each axis, the minimum (clamped at 0) and its axis, ties x < y < z
+// — the first step of Dda::setup / march's step selection (tracer.cpp:103-113).
+struct FaceCrossing {
+  std::array<double, 3> df;
+  double ds = 0.0;
+  int axis = 0;
+};
+FaceCrossing face_distances(const CartesianGrid& grid, const Vec3& pos, const Vec3& dir,
+                            int i, int j, int k);
 inline double geom_eps(const CartesianGrid& grid) {
   return 1e-12 * grid.min_spacing();
 }
@@ -248,6 +259,21 @@ struct SolutionField {
   std::int64_t total_steps = 0;
   double wall_time = 0.0;
 };
+
+// presample_and_sort (reference solver.hpp:39-50, solver.cpp:62-80): the
+// (band, g) of every ray of a cell from its keyed draws 2 and 3, ordered by
+// k(n, g, T_max) ascending (stable). Host utility; the GPU solve applies the
+// same order as its dispatch schedule (dispatch.cu), which never changes a
+// result.
+struct PlanEntry {
+  std::uint32_t ray_id = 0;
+  int band = 0;
+  int quad = 0;
+  double k_sort = 0.0;
+};
+std::vector<PlanEntry> presample_and_sort(std::uint64_t cell_id, std::uint32_t n_rays,
+                                          std::uint64_t seed, const SamplingCdfs& cdfs,
+                                          const SpectralModel& model);
 
 // Runs the whole solve on the GPU (ermc_b200_solve). Throws ermc::Error
 // with the reference's messages.

@@ -109,11 +109,14 @@ def build_pymod(force: bool = False, verbose: bool = True) -> Path:
 
 def build_oracle(verbose: bool = True) -> None:
     """Test-only checkers: the C restatement always; the reference library
-    (oracle/_ref) only where /root/reference exists (this container)."""
+    (oracle/_ref) and the reference's unit tests built against this library
+    (tests/_refcompat) only where /root/reference exists (this container)."""
     oracle = ROOT / "oracle"
     _run(["make", "-C", str(oracle), "oracle"], verbose)
     if Path("/root/reference/proj/src").is_dir():
         _run(["make", "-C", str(oracle), "-j8", "ref"], verbose)
+        # the reference's own unit tests compiled against the drop-in API
+        _run(["bash", str(ROOT / "tests" / "refcompat" / "build.sh")], verbose)
 
 
 def build(force: bool = False, verbose: bool = True) -> None:

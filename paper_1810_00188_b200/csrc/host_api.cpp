@@ -137,6 +137,28 @@ std::array<int, 3> locate(const CartesianGrid& grid, const Vec3& p,
 
 // ---------------------------------------------------------------- spectral
 
+FaceCrossing face_distances(const CartesianGrid& grid, const Vec3& pos, const Vec3& dir,
+                            int i, int j, int k) {
+  FaceCrossing fc;
+  const int idx[3] = {i, j, k};
+  for (int a = 0; a < 3; ++a) {
+    if (dir[a] == 0.0) {
+      fc.df[a] = kInf;
+      continue;
+    }
+    const double face = grid.origin[a] + (idx[a] + (dir[a] > 0.0 ? 1 : 0)) * grid.spacing(a);
+    fc.df[a] = (face - pos[a]) / dir[a];
+  }
+  fc.ds = fc.df[0];
+  for (int a = 1; a < 3; ++a)
+    if (fc.df[a] < fc.ds) {
+      fc.ds = fc.df[a];
+      fc.axis = a;
+    }
+  fc.ds = std::max(fc.ds, 0.0);
+  return fc;
+}
+
 QuadratureSet QuadratureSet::gauss_legendre(int n) {
   if (n < 1) throw Error("gauss_legendre: need at least one point");
   QuadratureSet q;
@@ -547,6 +569,44 @@ SolutionField solve(const CartesianGrid& grid, const TemperatureField& field,
   out.total_steps = s.total_steps;
   out.wall_time = s.wall_time;
   return out;
+}
+
+namespace {
+// The keyed stream of sampling.cpp:13-29 (MurmurHash3 fmix64 chain).
+std::uint64_t fmix64(std::uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+double keyed_uniform(std::uint64_t seed, std::uint64_t cell, std::uint32_t ray,
+                     std::uint32_t draw) {
+  std::uint64_t h = fmix64(seed + 0x9e3779b97f4a7c15ULL);
+  h = fmix64(h ^ cell);
+  h = fmix64(h ^ ((static_cast<std::uint64_t>(ray) << 32) | draw));
+  return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+int cdf_index(const std::vector<double>& cdf, double u) {
+  const auto it = std::upper_bound(cdf.begin(), cdf.end(), u);
+  const int i = static_cast<int>(it - cdf.begin());
+  return std::min(i, static_cast<int>(cdf.size()) - 1);
+}
+}  // namespace
+
+std::vector<PlanEntry> presample_and_sort(std::uint64_t cell_id, std::uint32_t n_rays,
+                                          std::uint64_t seed, const SamplingCdfs& cdfs,
+                                          const SpectralModel& model) {
+  std::vector<PlanEntry> plan(n_rays);
+  for (std::uint32_t r = 0; r < n_rays; ++r) {
+    const int n = cdf_index(cdfs.band_cdf, keyed_uniform(seed, cell_id, r, 2));
+    const int g = cdf_index(cdfs.quad_cdf[n], keyed_uniform(seed, cell_id, r, 3));
+    plan[r] = PlanEntry{r, n, g, model.interp_k(n, g, cdfs.t_max)};
+  }
+  std::stable_sort(plan.begin(), plan.end(),
+                   [](const PlanEntry& a, const PlanEntry& b) { return a.k_sort < b.k_sort; });
+  return plan;
 }
 
 // Line-by-line model (reference oracles.cpp:232-264): every spectral sample

@@ -267,3 +267,37 @@ def test_edge_sizes_match_reference():
         (q, sd, steps, total, _), (rq, rsd, rsteps, rtotal, _) = _solve_both(g, tt, bb, m, cfg)
         assert total == rtotal, shape
         assert_fp64_parity(q, rq, sd, rsd)
+
+
+def _solve_in_subprocess(env_extra, name, n, rays, seed, precision):
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = (
+        "import sys, json, numpy as np\n"
+        f"sys.path[:0] = [{str(root)!r}, {str(root / 'oracle')!r}]\n"
+        "import refshim\n"
+        "from paper_1810_00188_b200 import capi\n"
+        f"g, t, b, m, _ = refshim.ref_case({name!r}, {n})\n"
+        f"q, sd, st, tot, _ = capi.solve(g, t, b, m, capi.config_struct(rays_per_cell={rays}, "
+        f"seed={seed}, precision={precision}))\n"
+        "print(json.dumps([q.tobytes().hex(), sd.tobytes().hex(), int(tot)]))\n")
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         check=True).stdout.strip().splitlines()[-1]
+    return json.loads(out)
+
+
+@pytest.mark.parametrize("precision", [capi.FP64, capi.FP32])
+def test_dispatch_order_never_changes_results(precision):
+    # The narrow-band sorted dispatch (dispatch.cu) and its direction bins only
+    # reorder the marching: byte-identical Q_r / sigma / steps with the sort
+    # off, on, and on with 1 or 32 direction bins (P5 for the GPU schedule).
+    runs = [_solve_in_subprocess(env, "nb-parab", 10, 48, 31, precision)
+            for env in ({"ERMC_SORT": "0"}, {"ERMC_SORT": "1", "ERMC_SORT_DIRS": "1"},
+                        {"ERMC_SORT": "1", "ERMC_SORT_DIRS": "32"},
+                        {"ERMC_SORT": "1", "ERMC_SORT_TILE": "1000"})]
+    assert all(r == runs[0] for r in runs[1:])

@@ -25,7 +25,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__cycles_active.avg", "sm__cycles_elapsed.avg.per_second",
         "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
         "l1tex__throughput.avg.pct_of_peak_sustained_active",
-        "sm__warps_active.avg.pct_of_peak_sustained_active"]
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sectors.sum", "lts__t_sectors_srcunit_tex.sum"]
 UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 
 
@@ -67,6 +68,13 @@ def main():
                          "duration_ms": float(m["gpu__time_duration.sum"][0]),
                          "issue_active_pct": float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
                          "registers": int(float(m["launch__registers_per_thread"][0]))}
+        if "lts__t_sectors.sum" in m:
+            l2 = float(m["lts__t_sectors.sum"][0].replace(",", "")) * 32.0
+            ms = float(m["gpu__time_duration.sum"][0])
+            summary[prec].update(l2_bytes_per_step=l2 / steps, l2_gb_per_s=l2 / (ms * 1e-3) / 1e9,
+                                 dram_gb_per_s=dram / (ms * 1e-3) / 1e9,
+                                 thread_efficiency=float(m[
+                                     "smsp__thread_inst_executed_per_inst_executed.ratio"][0]) / 32)
     summary_path.write_text(json.dumps(summary, indent=1) + "\n")
     print(json.dumps(summary, indent=1))
 
