@@ -286,6 +286,7 @@ struct Tune {
   int sort = 1;  // narrow-band sorted dispatch (dispatch.cu)
   int track_pos = 0;  // 1 forces the position-tracking fp64 kernel
   int tint_arith = 1;  // compute exact-uniform temperature records (fp64)
+  int cdf_smem = 1;    // stage the sampling CDFs in shared memory (lean kernels)
   int sort_tile_items = 1 << 16;
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
 };
@@ -307,6 +308,7 @@ const Tune& tune() {
     x.sort = env_int("ERMC_SORT", x.sort);
     x.track_pos = env_int("ERMC_TRACK_POS", x.track_pos);
     x.tint_arith = env_int("ERMC_TINT_ARITH", x.tint_arith);
+    x.cdf_smem = env_int("ERMC_CDF_SMEM", x.cdf_smem);
     x.sort_tile_items = std::max(1, env_int("ERMC_SORT_TILE", x.sort_tile_items));
     x.sort_dirs = std::max(1, env_int("ERMC_SORT_DIRS", x.sort_dirs));
     return x;
@@ -683,6 +685,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.t_first = v.temps[0];
   P.t_last = v.temps[v.nt - 1];
   P.steps_per_level = s->d_steps.p;
+  P.cdf_smem = tune().cdf_smem && v.nb * (1 + v.nq) <= ermc_dev::kMaxSmemCdf ? 1 : 0;
   // Positions matter after a wall only if some wall can reflect.
   P.track_pos = 0;
   for (int a = 0; a < 3; ++a)

@@ -121,6 +121,42 @@ __device__ __forceinline__ int upper_bound_d(const double* a, int n, double x) {
   return first;
 }
 
+// std::upper_bound over an array in shared or global memory (generic loads).
+__device__ __forceinline__ int upper_bound_gen(const double* a, int n, double x) {
+  int first = 0, count = n;
+  while (count > 0) {
+    const int step = count >> 1;
+    if (!(x < a[first + step])) {
+      first += step + 1;
+      count -= step + 1;
+    } else {
+      count = step;
+    }
+  }
+  return first;
+}
+
+// Band / g CDFs staged in shared memory by the lean trace kernels when they
+// fit (P.cdf_smem): init's two binary searches then cost shared-memory
+// latency instead of dependent global loads. Layout: band_cdf[nb] then
+// quad_cdf[nb][nq], right after the kernel's per-thread records.
+
+__device__ __forceinline__ void stage_cdfs(const TraceParams& P, double* dst) {
+  const int nb = P.n_bands, n = nb + nb * P.n_quad;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    dst[i] = i < nb ? P.band_cdf[i] : P.quad_cdf[i - nb];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void sample_band_cdf(const TraceParams& P, const double* cdf,
+                                                double r_n, double r_g, int& n, int& g) {
+  const int nb = P.n_bands, nq = P.n_quad;
+  n = upper_bound_gen(cdf, nb, r_n);
+  if (n >= nb) n = nb - 1;
+  g = upper_bound_gen(cdf + nb + n * nq, nq, r_g);
+  if (g >= nq) g = nq - 1;
+}
+
 // sample_band (reference sampling.cpp:42-53).
 __device__ __forceinline__ void sample_band(const TraceParams& P, double r_n,
                                             double r_g, int& n, int& g) {

@@ -12,6 +12,8 @@
 namespace ermc_dev {
 
 constexpr int kMaxLevels = 16;
+constexpr int kMaxSmemCdf = 2048;  // sampling CDFs staged in shared memory up to
+                                   // this many doubles (16 KB; 119 x 16 needs 2023)
 
 // One multigrid level (reference GridHierarchy, geometry.hpp:74-83).
 struct LevelDesc {
@@ -63,6 +65,7 @@ struct TraceParams {
   const double4* iv64;       // [n_bands*n_quad][n_temps-1] {k_lo, k_hi, ib_lo, ib_hi}
   double inv_dt;             // 1/dt for the table-index estimate
   double inv_w;              // RN(1 / dt): tint's reciprocal when tint_arith
+  int32_t cdf_smem;          // lean kernels stage the sampling CDFs in shared memory
   int32_t tint_arith;        // every node is exactly l*dt + t0 and every width
                              // exactly dt, so tint[l] is computed, not loaded
   double t_first, t_last;    // table range

@@ -89,7 +89,7 @@ struct Ray {
   const double* krow;
   const double* ibrow;
   int idx[3], stp[3];
-  int band, level, sal, steps;
+  int band, quad, level, sal, steps;
   uint32_t next_draw, ray_id;
   uint64_t h_cell;
 };
@@ -123,9 +123,11 @@ __device__ __forceinline__ void dda_setup(const LevelDesc& L, Ray& r) {
 
 // init_ray (reference sampling.cpp:55-96) for global cell `cell`, with the
 // level-0 grid. Returns an error code (0 = ok).
+// cdf: the staged sampling CDFs (lean kernels) or null for P's global copy.
 __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
                                         uint32_t ray_id, Ray& r,
-                                        const double* dir_override) {
+                                        const double* dir_override,
+                                        const double* cdf = nullptr) {
   const LevelDesc& L = P.lv[0];
   int ci, cj, ck;
   decode_cell(L, cell, ci, cj, ck);
@@ -153,8 +155,12 @@ __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
   }
 
   int n, g;
-  sample_band(P, r_n, r_g, n, g);
+  if (cdf)
+    sample_band_cdf(P, cdf, r_n, r_g, n, g);
+  else
+    sample_band(P, r_n, r_g, n, g);
   r.band = n;
+  r.quad = g;
   r.krow = P.k + (static_cast<int64_t>(n) * P.n_quad + g) * P.n_temps;
   r.ibrow = P.ib + static_cast<int64_t>(n) * P.n_temps;
 
@@ -765,8 +771,12 @@ struct Fp64Lean {
       const bool pos_dir = da > 0.0;
       const int face_idx = idx[a] + (pos_dir ? 1 : 0);
       const double face = L.origin[a] + face_idx * L.d[a];
-      tn[a] = (face - pos[a]) / da;
-      const double td = L.d[a] / fabs(da);
+      // (face - pos) / da and d / |da| from one correctly rounded reciprocal
+      // (div_rcp returns the correctly rounded quotient, bitwise the IEEE
+      // division; |da| >= ~1e-17 here, far from under/overflow).
+      const double rda = 1.0 / da;
+      tn[a] = div_rcp(face - pos[a], da, rda);
+      const double td = div_rcp(L.d[a], fabs(da), fabs(rda));
       ax[a * kBlock] = make_int4(__double2loint(td), __double2hiint(td),
                                  pos_dir ? stride[a] : -stride[a],
                                  pos_dir ? L.n[a] - 1 - idx[a] : idx[a]);
@@ -780,7 +790,9 @@ struct Fp64Lean {
     extern __shared__ int4 s_dyn[];
     ax = s_dyn + threadIdx.x;
     Ray r;
-    const int e = init_ray(P, cell, ray, r, nullptr);
+    const double* cdf =
+        P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock) : nullptr;
+    const int e = init_ray(P, cell, ray, r, nullptr, cdf);
     if (e != kErrNone) return e;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -793,8 +805,7 @@ struct Fp64Lean {
     last_ib2 = r.ib1;
     rib1 = 1.0 / r.ib1;
     pref = r.pref;
-    const int64_t ng = (r.krow - P.k) / P.n_temps;
-    row = static_cast<int>(ng * (P.n_temps - 1));
+    row = (r.band * P.n_quad + r.quad) * (P.n_temps - 1);
     steps_ = 0;
     lvl = 0;
     sal_ = 0;
@@ -1045,6 +1056,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
 template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
+  extern __shared__ int4 s_dyn[];
+  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<kHint, kBrick, kPos>, false>(P);
 }
 
@@ -1052,6 +1065,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
 template <int kMinBlocks>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
+  extern __shared__ int4 s_dyn[];
+  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<0, false, true, true>, true>(P);
 }
 
@@ -1274,7 +1289,9 @@ bool lean_path(const TraceParams& P) {
          P.lv[0].n[0] * static_cast<int64_t>(P.lv[0].n[1]) * P.lv[0].n[2] < (1LL << 31);
 }
 size_t fp64_smem(const TraceParams& P) {
-  return lean_path(P) ? kLeanRecs64 * kBlock * sizeof(int4) : 0;
+  if (!lean_path(P)) return 0;
+  return kLeanRecs64 * kBlock * sizeof(int4) +
+         (P.cdf_smem ? static_cast<size_t>(P.n_bands) * (1 + P.n_quad) * sizeof(double) : 0);
 }
 // min_blocks = 0 picks the measured best per variant (B200, 256^3 channel):
 // 8 blocks/SM for the black-wall tracer (64 registers + 128 B of L1-resident
