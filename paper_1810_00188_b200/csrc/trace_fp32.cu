@@ -58,6 +58,17 @@ __device__ __forceinline__ int locate32(const LevelDesc& C, int a, float p, floa
   return min(max(i, 0), C.n[a] - 1);
 }
 
+// Sampling CDFs staged after the lean kernels' 3 x kBlock32 per-axis records.
+constexpr int kRecs32 = 3;
+__device__ __forceinline__ const double* staged_cdf(const TraceParams& P) {
+  extern __shared__ int4 s_dyn[];
+  return P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kRecs32 * kBlock32) : nullptr;
+}
+__device__ __forceinline__ void stage_cdfs32(const TraceParams& P) {
+  extern __shared__ int4 s_dyn[];
+  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kRecs32 * kBlock32));
+}
+
 struct Fp32Tracer {
   float p0[3];   // position at s = 0
   float dir[3];
@@ -106,8 +117,9 @@ struct Fp32Tracer {
     s = 0.0f;
   }
 
+  // cdf: sampling CDFs staged in shared memory by the lean kernels, or null.
   __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
-                                      uint32_t ray) {
+                                      uint32_t ray, const double* cdf = nullptr) {
     const LevelDesc& L = P.lv[0];
     int ci, cj, ck;
     decode_cell(L, cell, ci, cj, ck);
@@ -126,7 +138,10 @@ struct Fp32Tracer {
     dir[1] = sin_t * sp;
     dir[2] = cos_t;
     int n, g;
-    sample_band(P, r_n, r_g, n, g);
+    if (cdf)
+      sample_band_cdf(P, cdf, r_n, r_g, n, g);
+    else
+      sample_band(P, r_n, r_g, n, g);
     band = n;
     const int nt1 = P.n_temps - 1;
     row = P.iv32 + (static_cast<int64_t>(n) * P.n_quad + g) * nt1;
@@ -381,7 +396,7 @@ struct Fp32Lean {
     extern __shared__ int4 s_dyn[];
     ax = s_dyn + threadIdx.x;
     Fp32Tracer base;
-    const int e = base.init(P, cell, ray);
+    const int e = base.init(P, cell, ray, staged_cdf(P));
     if (e != kErrNone) return e;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -620,7 +635,7 @@ struct Fp32Brick {
     axr = reinterpret_cast<int2*>(s_dyn) + threadIdx.x;
     axl = reinterpret_cast<int*>(reinterpret_cast<int2*>(s_dyn) + 3 * kBlock32) + threadIdx.x;
     Fp32Tracer base;
-    const int e = base.init(P, cell, ray);
+    const int e = base.init(P, cell, ray, staged_cdf(P));
     if (e != kErrNone) return e;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -777,6 +792,7 @@ struct Fp32Brick {
 template <int kMinBlocks, int kHint, bool kPos = true>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
+  stage_cdfs32(P);
   pool_kernel_body<Fp32Brick<kHint, kPos>, false>(P);
 }
 
@@ -799,6 +815,7 @@ __global__ void to_fp32_bricked(const double* __restrict__ src, float* __restric
 template <int kMinBlocks, int kHint>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_lean(const __grid_constant__ TraceParams P) {
+  stage_cdfs32(P);
   pool_kernel_body<Fp32Lean<kHint>, false>(P);
 }
 
@@ -806,6 +823,7 @@ __global__ void __launch_bounds__(kBlock32, kMinBlocks)
 template <int kMinBlocks>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_lean_mg(const __grid_constant__ TraceParams P) {
+  stage_cdfs32(P);
   pool_kernel_body<Fp32Lean<0, true>, true>(P);
 }
 
@@ -858,7 +876,9 @@ namespace {
 using TraceFn32 = void (*)(TraceParams);
 bool fp32_lean(const TraceParams& P) { return P.lean != 0; }
 size_t fp32_smem(const TraceParams& P) {
-  return fp32_lean(P) ? 3 * kBlock32 * sizeof(int4) : 0;
+  if (!fp32_lean(P)) return 0;
+  return kRecs32 * kBlock32 * sizeof(int4) +
+         (P.cdf_smem ? static_cast<size_t>(P.n_bands) * (1 + P.n_quad) * sizeof(double) : 0);
 }
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   // 8 blocks/SM (64 registers) measured best; 10 and 12 lose (0.98, 0.92x).

@@ -121,83 +121,6 @@ __device__ __forceinline__ void dda_setup(const LevelDesc& L, Ray& r) {
   }
 }
 
-// init_ray (reference sampling.cpp:55-96) for global cell `cell`, with the
-// level-0 grid. Returns an error code (0 = ok).
-// cdf: the staged sampling CDFs (lean kernels) or null for P's global copy.
-__device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
-                                        uint32_t ray_id, Ray& r,
-                                        const double* dir_override,
-                                        const double* cdf = nullptr) {
-  const LevelDesc& L = P.lv[0];
-  int ci, cj, ck;
-  decode_cell(L, cell, ci, cj, ck);
-  r.h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(cell));
-  r.ray_id = ray_id;
-  double r_theta = draw_u(r.h_cell, ray_id, 0);
-  double r_phi = draw_u(r.h_cell, ray_id, 1);
-  double r_n = draw_u(r.h_cell, ray_id, 2);
-  double r_g = draw_u(r.h_cell, ray_id, 3);
-  r.next_draw = 4;
-
-  // sample_direction (sampling.cpp:31-40)
-  double cos_t = 1.0 - 2.0 * r_theta;
-  double phi = 2.0 * kPiD * r_phi;
-  double sin_t = sqrt(fmax(0.0, 1.0 - cos_t * cos_t));
-  double sp, cp;
-  sincos(phi, &sp, &cp);
-  r.dir[0] = sin_t * cp;
-  r.dir[1] = sin_t * sp;
-  r.dir[2] = cos_t;
-  if (dir_override) {
-    r.dir[0] = dir_override[0];
-    r.dir[1] = dir_override[1];
-    r.dir[2] = dir_override[2];
-  }
-
-  int n, g;
-  if (cdf)
-    sample_band_cdf(P, cdf, r_n, r_g, n, g);
-  else
-    sample_band(P, r_n, r_g, n, g);
-  r.band = n;
-  r.quad = g;
-  r.krow = P.k + (static_cast<int64_t>(n) * P.n_quad + g) * P.n_temps;
-  r.ibrow = P.ib + static_cast<int64_t>(n) * P.n_temps;
-
-  // cell centre (geometry.hpp:28-31), optional volume sampling
-  r.idx[0] = ci;
-  r.idx[1] = cj;
-  r.idx[2] = ck;
-  r.pos[0] = L.origin[0] + (ci + 0.5) * L.d[0];
-  r.pos[1] = L.origin[1] + (cj + 0.5) * L.d[1];
-  r.pos[2] = L.origin[2] + (ck + 0.5) * L.d[2];
-  if (P.volume_sampling) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-      r.pos[a] += (draw_u(r.h_cell, ray_id, r.next_draw++) - 0.5) * L.d[a];
-  }
-
-  double t_cell = __ldg(L.field + cell);
-  int lo;
-  double frac;
-  if (!t_lookup(P, t_cell, lo, frac)) return kErrTableRange;
-  r.ib1 = interp_row(r.ibrow, lo, frac);
-  double k_max = __ldg(P.k_max + static_cast<int64_t>(n) * P.n_quad + g);
-  double ib_max = __ldg(P.ib_max + n);
-  if (k_max <= 0.0 || ib_max <= 0.0) return kErrTransparent;
-  r.pref = interp_row(r.krow, lo, frac) * r.ib1 / (k_max * ib_max);
-
-  // march() prologue (tracer.cpp:62-77)
-  r.tau = 1.0;
-  r.q = 0.0;
-  r.last_ib2 = r.ib1;
-  r.level = 0;
-  r.sal = 0;
-  r.steps = 0;
-  dda_setup(L, r);
-  return kErrNone;
-}
-
 // One iteration of march's loop (reference tracer.cpp:82-185).
 // kMulti enables the multigrid demotion branch (tracer.cpp:91-101).
 template <bool kMulti, bool kDebug>
@@ -486,6 +409,98 @@ __device__ __forceinline__ bool lookup_spec(const TraceParams& P, const double4*
   lo = l;
   frac = f;
   return true;
+}
+
+// init_ray (reference sampling.cpp:55-96) for global cell `cell`, with the
+// level-0 grid. Returns an error code (0 = ok).
+// cdf: the staged sampling CDFs (lean kernels) or null for P's global copy.
+// kLean: the lean tracers' variant — the table lookup runs on the packed
+// interval records (lookup_spec: same values), and the DDA setup is left to
+// the tracer, which builds its own per-axis records.
+template <bool kLean = false>
+__device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
+                                        uint32_t ray_id, Ray& r,
+                                        const double* dir_override,
+                                        const double* cdf = nullptr) {
+  const LevelDesc& L = P.lv[0];
+  int ci, cj, ck;
+  decode_cell(L, cell, ci, cj, ck);
+  r.h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(cell));
+  r.ray_id = ray_id;
+  double r_theta = draw_u(r.h_cell, ray_id, 0);
+  double r_phi = draw_u(r.h_cell, ray_id, 1);
+  double r_n = draw_u(r.h_cell, ray_id, 2);
+  double r_g = draw_u(r.h_cell, ray_id, 3);
+  r.next_draw = 4;
+
+  // sample_direction (sampling.cpp:31-40)
+  double cos_t = 1.0 - 2.0 * r_theta;
+  double phi = 2.0 * kPiD * r_phi;
+  double sin_t = sqrt(fmax(0.0, 1.0 - cos_t * cos_t));
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  r.dir[0] = sin_t * cp;
+  r.dir[1] = sin_t * sp;
+  r.dir[2] = cos_t;
+  if (dir_override) {
+    r.dir[0] = dir_override[0];
+    r.dir[1] = dir_override[1];
+    r.dir[2] = dir_override[2];
+  }
+
+  int n, g;
+  if (cdf)
+    sample_band_cdf(P, cdf, r_n, r_g, n, g);
+  else
+    sample_band(P, r_n, r_g, n, g);
+  r.band = n;
+  r.quad = g;
+  r.krow = P.k + (static_cast<int64_t>(n) * P.n_quad + g) * P.n_temps;
+  r.ibrow = P.ib + static_cast<int64_t>(n) * P.n_temps;
+
+  // cell centre (geometry.hpp:28-31), optional volume sampling
+  r.idx[0] = ci;
+  r.idx[1] = cj;
+  r.idx[2] = ck;
+  r.pos[0] = L.origin[0] + (ci + 0.5) * L.d[0];
+  r.pos[1] = L.origin[1] + (cj + 0.5) * L.d[1];
+  r.pos[2] = L.origin[2] + (ck + 0.5) * L.d[2];
+  if (P.volume_sampling) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      r.pos[a] += (draw_u(r.h_cell, ray_id, r.next_draw++) - 0.5) * L.d[a];
+  }
+
+  double t_cell = __ldg(L.field + cell);
+  int lo;
+  double frac;
+  double k1;
+  if (kLean) {
+    double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}: copies of the table values
+    if (!lookup_spec<0>(P, P.iv64 + (n * P.n_quad + g) * (P.n_temps - 1), t_cell, lo, frac,
+                        v))
+      return kErrTableRange;
+    r.ib1 = frac == 0.0 ? v.z : v.z + frac * (v.w - v.z);
+    k1 = frac == 0.0 ? v.x : v.x + frac * (v.y - v.x);
+  } else {
+    if (!t_lookup(P, t_cell, lo, frac)) return kErrTableRange;
+    r.ib1 = interp_row(r.ibrow, lo, frac);
+    k1 = interp_row(r.krow, lo, frac);
+  }
+  double k_max = __ldg(P.k_max + static_cast<int64_t>(n) * P.n_quad + g);
+  double ib_max = __ldg(P.ib_max + n);
+  if (k_max <= 0.0 || ib_max <= 0.0) return kErrTransparent;
+  r.pref = k1 * r.ib1 / (k_max * ib_max);
+
+  // march() prologue (tracer.cpp:62-77)
+  r.tau = 1.0;
+  r.q = 0.0;
+  r.last_ib2 = r.ib1;
+  r.level = 0;
+  r.sal = 0;
+  r.steps = 0;
+  if (!kLean) dda_setup(L, r);
+  return kErrNone;
 }
 
 struct Fp64Fast {
@@ -792,7 +807,7 @@ struct Fp64Lean {
     Ray r;
     const double* cdf =
         P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock) : nullptr;
-    const int e = init_ray(P, cell, ray, r, nullptr, cdf);
+    const int e = init_ray<true>(P, cell, ray, r, nullptr, cdf);
     if (e != kErrNone) return e;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
