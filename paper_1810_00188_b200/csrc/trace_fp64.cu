@@ -753,7 +753,9 @@ __device__ __forceinline__ double expm1_lean(double x) {
 // the field pointer are then the coarse level's.
 constexpr int kLeanRecs64 = 4;
 
-template <int kHint, bool kBrick, bool kPos = true, bool kMulti = false>
+// kReflect = false (every wall black) drops the reflection code; the
+// multigrid tracer keeps positions for demotion but can still drop it.
+template <int kHint, bool kBrick, bool kPos = true, bool kMulti = false, bool kReflect = kPos>
 struct Fp64Lean {
   static_assert(!kMulti || (kPos && !kBrick), "demotion reads positions, k-fastest levels");
   double pos[3], dir[3], tn[3];
@@ -969,7 +971,7 @@ struct Fp64Lean {
     // ending the ray then leaves the report to the pool's finite-state check,
     // and with no reflection code the position and direction are dead after
     // setup (12 registers).
-    if (!kPos) return kDone;
+    if (!kReflect) return kDone;
     int idx[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);
@@ -1077,12 +1079,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
 }
 
 // Multigrid variant of the lean tracer (n_levels > 1).
-template <int kMinBlocks>
+template <int kMinBlocks, bool kReflect = true>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
-  pool_kernel_body<Fp64Lean<0, false, true, true>, true>(P);
+  pool_kernel_body<Fp64Lean<0, false, true, true, kReflect>, true>(P);
 }
 
 // Copies the fp64 k-fastest field into the 2x2x2 micro-brick layout.
@@ -1319,8 +1321,13 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   const bool brick = P.brick && P.lv[0].field64b;
   if (min_blocks <= 0) min_blocks = P.n_levels > 1 ? 6 : !P.track_pos ? 8 : 7;
   min_blocks = min(max(min_blocks, 6), 8);
-  if (P.n_levels > 1)
+  if (P.n_levels > 1) {
+    if (!P.track_pos)  // black walls: no reflection code
+      return min_blocks >= 8   ? trace_pool_fp64_lean_mg<8, false>
+             : min_blocks == 7 ? trace_pool_fp64_lean_mg<7, false>
+                               : trace_pool_fp64_lean_mg<6, false>;
     return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7> : trace_pool_fp64_lean_mg<6>;
+  }
   if (!P.track_pos) {
     if (brick) return trace_pool_fp64_lean<8, 0, true, false>;
     return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, false>
