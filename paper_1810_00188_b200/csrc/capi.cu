@@ -631,6 +631,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
     for (int a = 0; a < 3; ++a) {
       L.n[a] = count(g, a);
       L.d[a] = spacing(g, a);
+      L.rd[a] = 1.0 / L.d[a];
       L.origin[a] = g.origin[a];
       L.extent[a] = count(g, a) * spacing(g, a);
     }

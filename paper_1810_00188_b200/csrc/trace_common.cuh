@@ -20,6 +20,7 @@ struct LevelDesc {
   int32_t n[3];      // cells per axis
   int32_t cap;       // steps before demotion; -1 = uncapped (coarsest level)
   double d[3];       // spacing per axis
+  double rd[3];      // RN(1 / spacing): Markstein divisions by the spacing
   double origin[3];  // grid origin
   double extent[3];  // n * d, computed as CartesianGrid::extent
   double eps;        // geom_eps = 1e-12 * min spacing (geometry.hpp:114-116)

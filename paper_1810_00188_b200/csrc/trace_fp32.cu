@@ -339,7 +339,8 @@ struct Fp32Tracer {
 // loads of a register-only DDA; `lin` carries the cell index.
 // kMulti: multigrid ray coarsening (tracer.cpp:91-101) with Fp32Tracer's
 // demotion arithmetic; the records and field pointer then follow the level.
-template <int kHint, bool kMulti = false>
+// kReflect = false (every wall black): no reflection code.
+template <int kHint, bool kMulti = false, bool kReflect = true>
 struct Fp32Lean {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
@@ -509,6 +510,7 @@ struct Fp32Lean {
     acc = fmaf(tw, ibw - ib1n, acc);
     tau -= tw;
     if (tau <= P.tol32) return kDone;
+    if (!kReflect) return kDone;  // black walls: tau is 0 here unless non-finite
     // reflection (tracer.cpp:167-182)
     int idx[3];
 #pragma unroll
@@ -820,11 +822,11 @@ __global__ void __launch_bounds__(kBlock32, kMinBlocks)
 }
 
 // Multigrid variant of the lean tracer (n_levels > 1).
-template <int kMinBlocks>
+template <int kMinBlocks, bool kReflect = true>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_lean_mg(const __grid_constant__ TraceParams P) {
   stage_cdfs32(P);
-  pool_kernel_body<Fp32Lean<0, true>, true>(P);
+  pool_kernel_body<Fp32Lean<0, true, kReflect>, true>(P);
 }
 
 struct Fp32Multi : Fp32Tracer {
@@ -883,8 +885,10 @@ size_t fp32_smem(const TraceParams& P) {
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   // 8 blocks/SM (64 registers) measured best; 10 and 12 lose (0.98, 0.92x).
   const bool eight = min_blocks >= 8;
-  if (fp32_lean(P) && P.n_levels > 1)
+  if (fp32_lean(P) && P.n_levels > 1) {
+    if (!P.track_pos) return eight ? trace_pool_fp32_lean_mg<8, false> : trace_pool_fp32_lean_mg<6, false>;
     return eight ? trace_pool_fp32_lean_mg<8> : trace_pool_fp32_lean_mg<6>;
+  }
   if (fp32_lean(P) && P.brick) {
     if (!P.track_pos)
       return eight ? trace_pool_fp32_brick<8, 0, false> : trace_pool_fp32_brick<6, 0, false>;

@@ -843,7 +843,7 @@ struct Fp64Lean {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double p = pos[a] + C.eps * dir[a];
-      const double rel = (p - C.origin[a]) / C.d[a];
+      const double rel = div_rcp(p - C.origin[a], C.d[a], C.rd[a]);  // == (p - o) / d
       int i = static_cast<int>(floor(rel));
       if (i < 0 || i >= C.n[a]) {
         if (rel >= -1e-9 && i < 0)
@@ -1319,7 +1319,7 @@ size_t fp64_smem(const TraceParams& P) {
 TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (!lean_path(P)) return nullptr;
   const bool brick = P.brick && P.lv[0].field64b;
-  if (min_blocks <= 0) min_blocks = P.n_levels > 1 ? 6 : !P.track_pos ? 8 : 7;
+  if (min_blocks <= 0) min_blocks = P.n_levels > 1 ? (P.track_pos ? 6 : 7) : !P.track_pos ? 8 : 7;
   min_blocks = min(max(min_blocks, 6), 8);
   if (P.n_levels > 1) {
     if (!P.track_pos)  // black walls: no reflection code
