@@ -276,7 +276,7 @@ struct Timing {
 // override them for experiments — they never change results).
 struct Tune {
   int inner_steps = 32;    // fp64 march steps per pool check
-  int inner_steps32 = 64;  // fp32
+  int inner_steps32 = 48;  // fp32
   int refill = 8;
   int fp64_min_blocks = 0;  // 0 = per-tracer default (trace_fp64.cu)
   int fp32_min_blocks = 8;

@@ -13,7 +13,7 @@ kernel, ray-cell steps/s, steps per ray, and the check that applies:
   c4  config 4: 256^3 non-grey channel (the bench workload), fp64 and fp32;
   c5  config 5: rays-per-cell sweep at 256^3 — max / median sigma and time
       vs R, with log-log slopes (expected -0.5 and ~1);
-  mg  multigrid ray coarsening (n_levels 1..4) on the config-4 field.
+  mg  multigrid ray coarsening (n_levels 1..7) on the config-4 field.
 Channel runs are checked per cell against the reference CPU solver
 (oracle/_ref, cell-subset replay — bitwise its solve() for those cells) on
 a stratified sample of cells; fp32 runs against the fp64 solve (3 sigma).
@@ -181,7 +181,7 @@ def main():
     if "mg" in which:
         g, t, b, m, _ = W.channel_case(256, "nongrey16")
         for prec in ("fp64", "fp32"):
-            for lv in (1, 2, 3, 4):
+            for lv in (1, 2, 3, 4, 5, 6, 7):
                 cfg = capi.config_struct(rays_per_cell=64, seed=2024, n_levels=lv,
                                          steps_per_level=5, coarsen_ratio=2,
                                          precision=capi.FP64 if prec == "fp64" else capi.FP32)
