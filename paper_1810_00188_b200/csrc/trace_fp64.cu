@@ -919,8 +919,12 @@ struct Fp64Lean {
     if (inside || periodic)
       t_next = ld_t64<kHint>((kBrick ? L.field64b : L.field) + nlin);
 
-    const double kappa = frac == 0.0 ? v.x : v.x + frac * (v.y - v.x);
-    const double ib2 = frac == 0.0 ? v.z : v.z + frac * (v.w - v.z);
+    // interp's frac == 0 shortcut (spectral.cpp:179-205) needs no select here:
+    // a + 0 * (b - a) == a for finite table values (k is validated finite; a
+    // non-finite Ib makes the step non-finite on either form, and such rays
+    // are re-traced by the reference-order debug tracer for the error).
+    const double kappa = v.x + frac * (v.y - v.x);
+    const double ib2 = v.z + frac * (v.w - v.z);
     const double alpha = -expm1_lean(-kappa * ds);
     last_ib2 = ib2;
     q += P.qe * tau * alpha * div_rcp(ib2 - ib1, ib1, rib1) * pref;
