@@ -64,8 +64,8 @@ cudaError_t launch_to_bricked64(const double* src, double* dst, int nx, int ny, 
 int sort_max_bins();
 int sort_max_tile_items();
 cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_rows,
-                           int dir_bins, int tile_cells, uint32_t* packed, uint32_t* perm,
-                           cudaStream_t s);
+                           int dir_bins, int tile_cells, int block, uint32_t* packed,
+                           uint32_t* perm, cudaStream_t s);
 }  // namespace ermc_dev
 
 using ermc::Error;
@@ -288,6 +288,7 @@ struct Tune {
   int tint_arith = 1;  // compute exact-uniform temperature records (fp64)
   int cdf_smem = 1;    // stage the sampling CDFs in shared memory (lean kernels)
   int sort_tile_items = 1 << 16;
+  int sort_block = 0;  // cubic sort tiles (edge in cells; 0 = linear tiles)
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
 };
 int env_int(const char* name, int fallback) {
@@ -311,6 +312,7 @@ const Tune& tune() {
     x.cdf_smem = env_int("ERMC_CDF_SMEM", x.cdf_smem);
     x.sort_tile_items = std::max(1, env_int("ERMC_SORT_TILE", x.sort_tile_items));
     x.sort_dirs = std::max(1, env_int("ERMC_SORT_DIRS", x.sort_dirs));
+    x.sort_block = std::max(0, env_int("ERMC_SORT_BLOCK", x.sort_block));
     return x;
   }();
   return t;
@@ -794,6 +796,10 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
       (1ull << 31) - 1, std::max<uint64_t>(s->qray_budget_bytes / item_bytes, R));
   int64_t chunk_cells = std::max<int64_t>(1, static_cast<int64_t>(max_items / R));
   chunk_cells = std::min<int64_t>(chunk_cells, std::max<int64_t>(total_cells, 1));
+  {  // whole x-planes per chunk when possible (cubic sort tiles need them)
+    const int64_t plane = static_cast<int64_t>(s->grid.ny) * s->grid.nz;
+    if (chunk_cells < total_cells && chunk_cells >= plane) chunk_cells -= chunk_cells % plane;
+  }
   const int64_t n_chunks = total_cells == 0 ? 0 : (total_cells + chunk_cells - 1) / chunk_cells;
   s->d_qray.ensure(static_cast<size_t>(chunk_cells) * R);
   const int n_rows = s->view.nb * s->view.nq;
@@ -801,9 +807,14 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
     s->d_keys.ensure(static_cast<size_t>(chunk_cells) * R);
     s->d_perm.ensure(static_cast<size_t>(chunk_cells) * R);
   }
-  // <= 2^16 work ids per sort tile (whole cells)
+  // <= 2^16 work ids per sort tile (whole cells); cubic tiles of the largest
+  // edge in {ERMC_SORT_BLOCK, /2, ...} with edge^3 * R <= 2^16 (0 = linear)
   const int tile_cells = std::max(
       1, std::min(tune().sort_tile_items, ermc_dev::sort_max_tile_items()) / R);
+  int sort_block = tune().sort_block;
+  while (sort_block > 1 &&
+         static_cast<int64_t>(sort_block) * sort_block * sort_block * R > (int64_t(1) << 16))
+    sort_block /= 2;
   s->d_counters.ensure(2 * std::max<int64_t>(n_chunks, 1));
   s->d_errcode.ensure(std::max<int64_t>(n_chunks, 1));
   cuda_check(cudaMemsetAsync(s->d_counters.p, 0,
@@ -835,7 +846,7 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
       cudaEventCreate(&ts[ch].b);
       cudaEventRecord(ts[ch].a, st);
       cuda_check(ermc_dev::launch_ng_sort(P, s->d_row_rank.p, n_rows, tune().sort_dirs,
-                                          tile_cells, s->d_keys.p,
+                                          tile_cells, sort_block, s->d_keys.p,
                                           s->d_perm.p, st),
                  "narrow-band sort");
       cudaEventRecord(ts[ch].b, st);

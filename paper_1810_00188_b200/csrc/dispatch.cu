@@ -60,9 +60,64 @@ __device__ __forceinline__ int upper_bound_any(const double* a, int n, double x)
 //   pass 2: perm[tile + offset[key] + rank] = id — no atomics.
 // Dynamic shared memory: n_bins counters, kSortBlock partial sums, and the
 // band / g CDFs when they fit (cdf_len > 0).
+// Tile geometry. Linear: tile t = work ids [t * items, (t + 1) * items).
+// Blocked (the chunk is whole x-planes): tile t = a bx^3 block of cells —
+// (tx, ty, tz) in x-major block order, clipped at the chunk's faces — so the
+// rays that share a spectral row and direction bin also start within a few
+// cells of each other and their temperature gathers share cache lines.
+struct TileGeom {
+  uint32_t items;     // linear: work ids per tile
+  int b;              // blocked: block edge (0 = linear tiles)
+  int nx, ny, nz;     // blocked: chunk planes, grid ny, nz
+  int nby, nbz;       // blocked: blocks along y, z
+};
+
+// Work id of item u of tile t, the tile's first dispatch position, its item
+// count.
+struct TileMap {
+  const TileGeom& g;
+  uint32_t rays;
+  uint32_t t;
+  int tx, ty, tz, cx, cy, cz;
+  __device__ TileMap(const TileGeom& geo, uint32_t r, uint32_t tile, uint32_t n_work)
+      : g(geo), rays(r), t(tile) {
+    if (g.b == 0) {
+      tx = ty = tz = cx = cy = cz = 0;
+      return;
+    }
+    tz = static_cast<int>(t % g.nbz);
+    ty = static_cast<int>((t / g.nbz) % g.nby);
+    tx = static_cast<int>(t / (g.nbz * g.nby));
+    cx = min(g.b, g.nx - tx * g.b);
+    cy = min(g.b, g.ny - ty * g.b);
+    cz = min(g.b, g.nz - tz * g.b);
+  }
+  __device__ uint32_t first(uint32_t n_work) const {
+    if (g.b == 0) return t * g.items;
+    const uint64_t cells = static_cast<uint64_t>(tx) * g.b * g.ny * g.nz +
+                           static_cast<uint64_t>(cx) * (static_cast<uint64_t>(ty) * g.b * g.nz +
+                                                        static_cast<uint64_t>(cy) * tz * g.b);
+    return static_cast<uint32_t>(cells * rays);
+  }
+  __device__ uint32_t count(uint32_t n_work) const {
+    if (g.b == 0) return min(n_work - t * g.items, g.items);
+    return static_cast<uint32_t>(cx * cy * cz) * rays;
+  }
+  __device__ uint32_t work(uint32_t u, uint32_t n_work) const {
+    if (g.b == 0) return t * g.items + u;
+    const uint32_t lc = u / rays, ray = u - lc * rays;
+    const int dk = static_cast<int>(lc % cz);
+    const int dj = static_cast<int>((lc / cz) % cy);
+    const int di = static_cast<int>(lc / (cz * cy));
+    const uint32_t cell = (static_cast<uint32_t>(tx * g.b + di) * g.ny + (ty * g.b + dj)) * g.nz +
+                          (tz * g.b + dk);
+    return cell * rays + ray;
+  }
+};
+
 __global__ void __launch_bounds__(kSortBlock)
     ng_tile_sort(const __grid_constant__ TraceParams P, const int32_t* __restrict__ row_rank,
-                 int n_bins, int dir_bins, int cdf_len, uint32_t tile_items,
+                 int n_bins, int dir_bins, int cdf_len, TileGeom geo,
                  uint32_t* __restrict__ packed,
                  uint32_t* __restrict__ perm) {
   extern __shared__ __align__(8) unsigned char s_raw[];
@@ -70,8 +125,10 @@ __global__ void __launch_bounds__(kSortBlock)
   unsigned int* s_cur = reinterpret_cast<unsigned int*>(s_raw + cdf_len * sizeof(double));
   unsigned int* s_part = s_cur + n_bins;
   const uint32_t n = static_cast<uint32_t>(P.n_work);
-  const uint32_t t0 = blockIdx.x * tile_items;
-  const uint32_t t1 = min(n, t0 + tile_items);
+  const uint32_t rays = static_cast<uint32_t>(P.rays);
+  const TileMap tm(geo, rays, blockIdx.x, n);
+  const uint32_t t0 = tm.first(n);
+  const uint32_t cnt = tm.count(n);
   const int nb = P.n_bands, nq = P.n_quad;
   for (int b = threadIdx.x; b < n_bins; b += blockDim.x) s_cur[b] = 0u;
   for (int b = threadIdx.x; b < cdf_len; b += blockDim.x)
@@ -79,8 +136,8 @@ __global__ void __launch_bounds__(kSortBlock)
   __syncthreads();
   const double* band_cdf = cdf_len ? s_cdf : P.band_cdf;
   const double* quad_cdf = cdf_len ? s_cdf + nb : P.quad_cdf;
-  const uint32_t rays = static_cast<uint32_t>(P.rays);
-  for (uint32_t w = t0 + threadIdx.x; w < t1; w += blockDim.x) {
+  for (uint32_t u = threadIdx.x; u < cnt; u += blockDim.x) {
+    const uint32_t w = tm.work(u, n);
     // sample_band on draws 2 and 3 of the ray's key (sampling.cpp:42-53, 77-78)
     const uint32_t c = w / rays;
     const uint32_t ray = w - c * rays;
@@ -130,7 +187,8 @@ __global__ void __launch_bounds__(kSortBlock)
     run += v;
   }
   __syncthreads();
-  for (uint32_t w = t0 + threadIdx.x; w < t1; w += blockDim.x) {
+  for (uint32_t u = threadIdx.x; u < cnt; u += blockDim.x) {
+    const uint32_t w = tm.work(u, n);
     const uint32_t kr = packed[w];
     perm[t0 + s_cur[kr >> 16] + (kr & 0xffffu)] = w;
   }
@@ -141,14 +199,28 @@ __global__ void __launch_bounds__(kSortBlock)
 int sort_max_bins() { return kMaxSortBins; }
 int sort_max_tile_items() { return 1 << 16; }
 
+// tile_cells: cells per linear tile; block: edge of the cubic tiles when the
+// chunk is whole x-planes (0 = linear tiles).
 cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_rows,
-                           int dir_bins, int tile_cells, uint32_t* packed, uint32_t* perm,
-                           cudaStream_t s) {
+                           int dir_bins, int tile_cells, int block, uint32_t* packed,
+                           uint32_t* perm, cudaStream_t s) {
   while (dir_bins > 1 && n_rows * dir_bins > kMaxSortBins) dir_bins /= 2;
   const int n_bins = n_rows * dir_bins;
   if (P.n_work == 0) return cudaSuccess;
-  const uint32_t tile_items = static_cast<uint32_t>(tile_cells) * static_cast<uint32_t>(P.rays);
+  const uint32_t rays = static_cast<uint32_t>(P.rays);
+  const uint32_t tile_items = static_cast<uint32_t>(tile_cells) * rays;
   if (n_bins > kMaxSortBins || tile_items > (1u << 16)) return cudaErrorInvalidValue;
+  TileGeom geo{tile_items, 0, 0, 0, 0, 0, 0};
+  const int64_t plane = static_cast<int64_t>(P.lv[0].n[1]) * P.lv[0].n[2];
+  if (block > 0 && P.cell_base % plane == 0 && P.n_cells % plane == 0 &&
+      static_cast<uint64_t>(block) * block * block * rays <= (1u << 16)) {
+    geo.b = block;
+    geo.nx = static_cast<int>(P.n_cells / plane);
+    geo.ny = P.lv[0].n[1];
+    geo.nz = P.lv[0].n[2];
+    geo.nby = (geo.ny + block - 1) / block;
+    geo.nbz = (geo.nz + block - 1) / block;
+  }
   const int cdf_total = P.n_bands + P.n_bands * P.n_quad;
   const int cdf_len = cdf_total <= 4096 ? cdf_total : 0;
   const size_t smem = cdf_len * sizeof(double) + (n_bins + kSortBlock) * sizeof(unsigned int);
@@ -158,9 +230,9 @@ cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_
     if (e != cudaSuccess) return e;
   }
   const uint32_t n = static_cast<uint32_t>(P.n_work);
-  const uint32_t tiles = (n + tile_items - 1) / tile_items;
-  ng_tile_sort<<<tiles, kSortBlock, smem, s>>>(P, row_rank, n_bins, dir_bins, cdf_len,
-                                               tile_items,
+  const uint32_t tiles = geo.b ? static_cast<uint32_t>((geo.nx + geo.b - 1) / geo.b) * geo.nby * geo.nbz
+                               : (n + tile_items - 1) / tile_items;
+  ng_tile_sort<<<tiles, kSortBlock, smem, s>>>(P, row_rank, n_bins, dir_bins, cdf_len, geo,
                                                packed, perm);
   return cudaGetLastError();
 }

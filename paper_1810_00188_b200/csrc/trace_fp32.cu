@@ -510,43 +510,46 @@ struct Fp32Lean {
     acc = fmaf(tw, ibw - ib1n, acc);
     tau -= tw;
     if (tau <= P.tol32) return kDone;
-    if (!kReflect) return kDone;  // black walls: tau is 0 here unless non-finite
-    // reflection (tracer.cpp:167-182)
-    int idx[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);  // rp->z still 0: the boundary cell
-    rebase();
-    const float face_pos =
-        static_cast<float>(L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
-    float nd[3] = {dir[0], dir[1], dir[2]};
-    if (P.specular) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (a == axis) nd[a] = -nd[a];
+    if constexpr (!kReflect) {  // black walls: tau is 0 here unless non-finite
+      return kDone;
     } else {
-      const double r1 = draw_u(h_cell, ray_id, next_draw++);
-      const double r2 = draw_u(h_cell, ray_id, next_draw++);
-      const float sin_t = sqrtf(static_cast<float>(r1));
-      const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
-      float sp, cp;
-      sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
-      const int t1 = axis == 2 ? 0 : axis + 1;
-      const int t2 = axis == 0 ? 2 : axis - 1;
-      const float inward = at_hi ? -1.0f : 1.0f;
+      // reflection (tracer.cpp:167-182)
+      int idx[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);  // rp->z still 0: the boundary cell
+      rebase();
+      const float face_pos =
+          static_cast<float>(L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
+      float nd[3] = {dir[0], dir[1], dir[2]};
+      if (P.specular) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (a == axis) nd[a] = -nd[a];
+      } else {
+        const double r1 = draw_u(h_cell, ray_id, next_draw++);
+        const double r2 = draw_u(h_cell, ray_id, next_draw++);
+        const float sin_t = sqrtf(static_cast<float>(r1));
+        const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
+        float sp, cp;
+        sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
+        const int t1 = axis == 2 ? 0 : axis + 1;
+        const int t2 = axis == 0 ? 2 : axis - 1;
+        const float inward = at_hi ? -1.0f : 1.0f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (a == axis) nd[a] = inward * cos_t;
+          if (a == t1) nd[a] = sin_t * cp;
+          if (a == t2) nd[a] = sin_t * sp;
+        }
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        if (a == axis) nd[a] = inward * cos_t;
-        if (a == t1) nd[a] = sin_t * cp;
-        if (a == t2) nd[a] = sin_t * sp;
+        if (a == axis) p0[a] = face_pos;
+        dir[a] = nd[a];
       }
+      setup(L, idx);
+      return kContinue;
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a == axis) p0[a] = face_pos;
-      dir[a] = nd[a];
-    }
-    setup(L, idx);
-    return kContinue;
   }
 
   __device__ __forceinline__ double finish(const TraceParams&) const {
@@ -741,43 +744,46 @@ struct Fp32Brick {
     acc = fmaf(tw, ibw - ib1n, acc);
     tau -= tw;
     if (tau <= P.tol32) return kDone;
-    if (!kPos) return kDone;  // black walls: tau is 0 here unless non-finite
-    // reflection (tracer.cpp:167-182)
-    int idx[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);  // left still 0: the boundary cell
-    rebase();
-    const float face_pos =
-        static_cast<float>(L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
-    float nd[3] = {dir[0], dir[1], dir[2]};
-    if (P.specular) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (a == axis) nd[a] = -nd[a];
+    if constexpr (!kPos) {  // black walls: tau is 0 here unless non-finite
+      return kDone;
     } else {
-      const double r1 = draw_u(h_cell, ray_id, next_draw++);
-      const double r2 = draw_u(h_cell, ray_id, next_draw++);
-      const float sin_t = sqrtf(static_cast<float>(r1));
-      const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
-      float sp, cp;
-      sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
-      const int t1 = axis == 2 ? 0 : axis + 1;
-      const int t2 = axis == 0 ? 2 : axis - 1;
-      const float inward = at_hi ? -1.0f : 1.0f;
+      // reflection (tracer.cpp:167-182)
+      int idx[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);  // left still 0: the boundary cell
+      rebase();
+      const float face_pos =
+          static_cast<float>(L.origin[axis] + (at_hi ? L.extent[axis] : 0.0));
+      float nd[3] = {dir[0], dir[1], dir[2]};
+      if (P.specular) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (a == axis) nd[a] = -nd[a];
+      } else {
+        const double r1 = draw_u(h_cell, ray_id, next_draw++);
+        const double r2 = draw_u(h_cell, ray_id, next_draw++);
+        const float sin_t = sqrtf(static_cast<float>(r1));
+        const float cos_t = sqrtf(static_cast<float>(1.0 - r1));
+        float sp, cp;
+        sincospif(static_cast<float>(2.0 * r2), &sp, &cp);
+        const int t1 = axis == 2 ? 0 : axis + 1;
+        const int t2 = axis == 0 ? 2 : axis - 1;
+        const float inward = at_hi ? -1.0f : 1.0f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (a == axis) nd[a] = inward * cos_t;
+          if (a == t1) nd[a] = sin_t * cp;
+          if (a == t2) nd[a] = sin_t * sp;
+        }
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        if (a == axis) nd[a] = inward * cos_t;
-        if (a == t1) nd[a] = sin_t * cp;
-        if (a == t2) nd[a] = sin_t * sp;
+        if (a == axis) p0[a] = face_pos;
+        dir[a] = nd[a];
       }
+      setup(L, idx);
+      return kContinue;
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a == axis) p0[a] = face_pos;
-      dir[a] = nd[a];
-    }
-    setup(L, idx);
-    return kContinue;
   }
 
   __device__ __forceinline__ double finish(const TraceParams&) const {

@@ -975,48 +975,51 @@ struct Fp64Lean {
     // ending the ray then leaves the report to the pool's finite-state check,
     // and with no reflection code the position and direction are dead after
     // setup (12 registers).
-    if (!kReflect) return kDone;
-    int idx[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);
-    const double face_pos = L.origin[axis] + (at_hi ? L.extent[axis] : 0.0);
-    const int inward = at_hi ? -1 : 1;
-    double nd[3] = {dir[0], dir[1], dir[2]};
-    if (P.specular) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (a == axis) nd[a] = -nd[a];
+    if constexpr (!kReflect) {
+      return kDone;
     } else {
-      const uint64_t h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(r3.z));
-      const uint32_t ray_id = static_cast<uint32_t>(r3.w);
-      const uint32_t draw0 = static_cast<uint32_t>(r3.y);
-      const double r1 = draw_u(h_cell, ray_id, draw0);
-      const double r2 = draw_u(h_cell, ray_id, draw0 + 1);
-      ax[3 * kBlock].y = static_cast<int>(draw0 + 2);
-      const double sin_t = sqrt(r1);
-      const double cos_t = sqrt(1.0 - r1);
-      const double phi = 2.0 * kPiD * r2;
-      double sp, cp;
-      sincos(phi, &sp, &cp);
-      const int t1 = axis == 2 ? 0 : axis + 1;
-      const int t2 = axis == 0 ? 2 : axis - 1;
+      int idx[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) idx[a] = idx_of(L, a);
+      const double face_pos = L.origin[axis] + (at_hi ? L.extent[axis] : 0.0);
+      const int inward = at_hi ? -1 : 1;
+      double nd[3] = {dir[0], dir[1], dir[2]};
+      if (P.specular) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (a == axis) nd[a] = -nd[a];
+      } else {
+        const uint64_t h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(r3.z));
+        const uint32_t ray_id = static_cast<uint32_t>(r3.w);
+        const uint32_t draw0 = static_cast<uint32_t>(r3.y);
+        const double r1 = draw_u(h_cell, ray_id, draw0);
+        const double r2 = draw_u(h_cell, ray_id, draw0 + 1);
+        ax[3 * kBlock].y = static_cast<int>(draw0 + 2);
+        const double sin_t = sqrt(r1);
+        const double cos_t = sqrt(1.0 - r1);
+        const double phi = 2.0 * kPiD * r2;
+        double sp, cp;
+        sincos(phi, &sp, &cp);
+        const int t1 = axis == 2 ? 0 : axis + 1;
+        const int t2 = axis == 0 ? 2 : axis - 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (a == axis) nd[a] = inward * cos_t;
+          if (a == t1) nd[a] = sin_t * cp;
+          if (a == t2) nd[a] = sin_t * sp;
+        }
+      }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        if (a == axis) nd[a] = inward * cos_t;
-        if (a == t1) nd[a] = sin_t * cp;
-        if (a == t2) nd[a] = sin_t * sp;
+        if (a == axis) pos[a] = face_pos;
+        dir[a] = nd[a];
       }
+      pos[0] += L.eps * dir[0];
+      pos[1] += L.eps * dir[1];
+      pos[2] += L.eps * dir[2];
+      setup(L, idx);
+      return kContinue;
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a == axis) pos[a] = face_pos;
-      dir[a] = nd[a];
-    }
-    pos[0] += L.eps * dir[0];
-    pos[1] += L.eps * dir[1];
-    pos[2] += L.eps * dir[2];
-    setup(L, idx);
-    return kContinue;
   }
 
   __device__ __forceinline__ double finish(const TraceParams& P) const {
@@ -1048,11 +1051,6 @@ struct Fp64Tracer {
   __device__ __forceinline__ int level() const { return r.level; }
   __device__ __forceinline__ int sal() const { return r.sal; }
   __device__ __forceinline__ int steps() const { return r.steps; }
-};
-struct Fp64Single : Fp64Tracer {
-  __device__ __forceinline__ int step(const TraceParams& P, int m) {
-    return step_t<false>(P, m);
-  }
 };
 struct Fp64Multi : Fp64Tracer {
   __device__ __forceinline__ int step(const TraceParams& P, int m) {

@@ -299,5 +299,7 @@ def test_dispatch_order_never_changes_results(precision):
     runs = [_solve_in_subprocess(env, "nb-parab", 10, 48, 31, precision)
             for env in ({"ERMC_SORT": "0"}, {"ERMC_SORT": "1", "ERMC_SORT_DIRS": "1"},
                         {"ERMC_SORT": "1", "ERMC_SORT_DIRS": "32"},
-                        {"ERMC_SORT": "1", "ERMC_SORT_TILE": "1000"})]
+                        {"ERMC_SORT": "1", "ERMC_SORT_TILE": "1000"},
+                        {"ERMC_SORT": "1", "ERMC_SORT_BLOCK": "8"},  # cubic tiles, clipped
+                        {"ERMC_SORT": "1", "ERMC_SORT_BLOCK": "4"})]
     assert all(r == runs[0] for r in runs[1:])
