@@ -1,0 +1,26 @@
+#!/bin/bash
+# compute-sanitizer memcheck / racecheck over small solves of every tracer.
+OUT=gpurun_out; mkdir -p $OUT
+CS=/usr/local/cuda/bin/compute-sanitizer
+cat > /tmp/san_case.py <<'PY'
+import sys
+sys.path[:0] = ["ROOT", "ROOT/oracle", "ROOT/tests"]
+import numpy as np, refshim
+from paper_1810_00188_b200 import capi, workloads as W
+cases = [("nb-parab", 10, {}), ("epsw-low", 9, {}), ("nb-3dimens", 10, dict(n_levels=3, steps_per_level=3)),
+         ("box-sin-5", 8, dict(specular_walls=1)), ("grey-parab", 8, dict(volume_sampling=1))]
+for name, n, v in cases:
+    g, t, b, m, _ = refshim.ref_case(name, n)
+    for prec in (capi.FP64, capi.FP32):
+        capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec, **v))
+        capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec, **v), cell_range=(7, 300))
+g, t, b, m = W.channel_case(16, "nongrey16")[:4]
+for prec in (capi.FP64, capi.FP32):
+    capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec, n_devices=2))
+print("sanitizer cases done")
+PY
+sed -i "s#ROOT#$PWD#g" /tmp/san_case.py
+timeout 1500 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_memcheck.txt 2>&1; echo "memcheck rc=$?" >> $OUT/sanitize_memcheck.txt
+ERMC_SORT_BLOCK=8 timeout 1500 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_memcheck_blk.txt 2>&1; echo "memcheck rc=$?" >> $OUT/sanitize_memcheck_blk.txt
+timeout 1500 $CS --tool racecheck --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_racecheck.txt 2>&1; echo "racecheck rc=$?" >> $OUT/sanitize_racecheck.txt
+tail -3 $OUT/sanitize_memcheck.txt $OUT/sanitize_memcheck_blk.txt $OUT/sanitize_racecheck.txt
