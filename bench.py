@@ -272,6 +272,30 @@ def run_b200(a, world, rank, local):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     t_dev = torch.from_numpy(t_host).to(dev)
 
+    # N > 1: how Q_r / sigma are assembled on every rank. "fused" (default):
+    # the solve's reduction kernel stores each cell straight into every rank's
+    # full-field buffer (CUDA IPC mappings; NVLink stores), no collective after
+    # the solve. "nccl": all-gather of the slabs. ERMC_BENCH_GATHER overrides;
+    # if the IPC mappings cannot be made the run uses NCCL and says so.
+    gather = os.environ.get("ERMC_BENCH_GATHER", "fused") if world > 1 else "none"
+    outs = None
+    if gather == "fused":
+        try:
+            q_full = capi.device_alloc(local, n_cells * 8)
+            sd_full = capi.device_alloc(local, n_cells * 8)
+            handles = [None] * world
+            dist.all_gather_object(handles, (capi.ipc_export(q_full), capi.ipc_export(sd_full)))
+            outs = ([q_full if r == rank else capi.ipc_open(handles[r][0]) for r in range(world)],
+                    [sd_full if r == rank else capi.ipc_open(handles[r][1]) for r in range(world)])
+            ok = 1
+        except Exception as exc:  # pragma: no cover - depends on the node
+            ok = 0
+            sys.stderr.write(f"fused gather unavailable: {exc}\n")
+        flag = torch.tensor([ok], dtype=torch.int64, device=cdev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            gather, outs = "nccl (fused unavailable)", None
+
     def device_resident(precision, steps, warmup):
         cfg = capi.config_struct(rays_per_cell=a.rays, seed=a.seed, precision=precision,
                                  device=local)
@@ -283,6 +307,8 @@ def run_b200(a, world, rank, local):
 
         def one():
             flush.zero_()
+            if outs is not None:  # reduction writes every rank's full field
+                return sess.solve_scatter(slab.lo, slab.hi, outs[0], outs[1], sptr)
             st = sess.solve(slab.lo, slab.hi, q.data_ptr(), sd.data_ptr(), sptr)
             if world > 1:
                 parallel.gather_slabs(q, slabs, dist)
@@ -402,8 +428,10 @@ def run_b200(a, world, rank, local):
                     "generated through the solver API)",
             "config": {"workload": workload_name(a), "grid": a.grid, "rays_per_cell": a.rays,
                        "model": a.model, "precision": a.precision,
-                       "parallelism": f"x-slabs x{world}" + (f" + {backend} all-gather" if world > 1
-                                                             else ""),
+                       "parallelism": f"x-slabs x{world}" + (
+                           "" if world == 1 else
+                           " + all-gather fused into the reduction (CUDA IPC, NVLink stores)"
+                           if gather == "fused" else f" + {backend} all-gather"),
                        "l2": "flushed (256 MiB write) before every step"},
             "s_per_field": el_max * 1e-3 / a.steps,
             "steps_per_field": steps_per_field,

@@ -163,6 +163,30 @@ int ermc_b200_session_solve(ermc_session_t* s, int64_t cell_lo,
                             int64_t* steps_per_level, void* stream,
                             char* errbuf, size_t errlen);
 
+/* session_solve with the all-gather fused into the per-cell reduction: each
+ * cell's Q_r / sigma is stored into all n_out (<= 8) full-field buffers —
+ * this device's and peer GPUs' (mapped with ermc_b200_ipc_open) — at its
+ * global linear index, by the reduction kernel itself (NVLink stores on a
+ * B200 node). After every rank's call and a barrier each buffer holds the
+ * whole field. Replaces the reference's single-process result assembly. */
+int ermc_b200_session_solve_scatter(ermc_session_t* s, int64_t cell_lo,
+                                    int64_t cell_hi, double* const* d_q_full,
+                                    double* const* d_sd_full, int32_t n_out,
+                                    int64_t* steps_per_level, void* stream,
+                                    char* errbuf, size_t errlen);
+
+/* Device buffers shareable across processes (cudaMalloc'd, so their CUDA IPC
+ * handles address the buffer itself). */
+int ermc_b200_device_alloc(int device, size_t bytes, void** d_ptr, char* errbuf,
+                           size_t errlen);
+int ermc_b200_device_free(void* d_ptr);
+/* CUDA IPC export / map / unmap of such a buffer (64-byte handles). */
+int ermc_b200_ipc_export(const void* d_ptr, uint8_t handle[64], char* errbuf,
+                         size_t errlen);
+int ermc_b200_ipc_open(const uint8_t handle[64], void** d_ptr, char* errbuf,
+                       size_t errlen);
+int ermc_b200_ipc_close(void* d_ptr);
+
 /* Per-kernel device times (CUDA events on the launch stream) of the last
  * session_solve, milliseconds: [0] validate+T_max, [1] restrict + the
  * narrow-band sort of the dispatch order, [2] trace (all chunks),

@@ -88,6 +88,17 @@ EXPORTS = {
                                           C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
                                           C.c_char_p, C.c_size_t]),
     "ermc_b200_session_timings": (C.c_int, [C.c_void_p, _d, C.POINTER(C.c_int32)]),
+    "ermc_b200_session_solve_scatter": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64,
+                                                  C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                                  C.c_int32, C.POINTER(C.c_int64), C.c_void_p,
+                                                  C.c_char_p, C.c_size_t]),
+    "ermc_b200_device_alloc": (C.c_int, [C.c_int, C.c_size_t, C.POINTER(C.c_void_p), C.c_char_p,
+                                         C.c_size_t]),
+    "ermc_b200_device_free": (C.c_int, [C.c_void_p]),
+    "ermc_b200_ipc_export": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_char_p, C.c_size_t]),
+    "ermc_b200_ipc_open": (C.c_int, [C.POINTER(C.c_uint8), C.POINTER(C.c_void_p), C.c_char_p,
+                                     C.c_size_t]),
+    "ermc_b200_ipc_close": (C.c_int, [C.c_void_p]),
     "ermc_b200_trace_rays": (C.c_int, [C.POINTER(Grid), _d, C.POINTER(Boundary),
                                        C.POINTER(Model), C.POINTER(Config), C.c_double,
                                        C.c_double, C.c_int64, C.POINTER(C.c_int64),
@@ -292,6 +303,31 @@ def planck_mean(model: ModelArrays, t: float) -> float:
     return out.value
 
 
+def device_alloc(device: int, nbytes: int) -> int:
+    lib = load()
+    p = C.c_void_p()
+    buf = _err()
+    _raise(lib.ermc_b200_device_alloc(device, nbytes, C.byref(p), buf, len(buf)), buf)
+    return p.value
+
+
+def ipc_export(ptr: int) -> bytes:
+    lib = load()
+    h = (C.c_uint8 * 64)()
+    buf = _err()
+    _raise(lib.ermc_b200_ipc_export(C.c_void_p(ptr), h, buf, len(buf)), buf)
+    return bytes(h)
+
+
+def ipc_open(handle: bytes) -> int:
+    lib = load()
+    h = (C.c_uint8 * 64)(*handle)
+    p = C.c_void_p()
+    buf = _err()
+    _raise(lib.ermc_b200_ipc_open(h, C.byref(p), buf, len(buf)), buf)
+    return p.value
+
+
 def uniform_device(seed: int, cells, rays, draws) -> np.ndarray:
     lib = load()
     cells = np.ascontiguousarray(cells, dtype=np.uint64)
@@ -332,6 +368,20 @@ class Session:
         _raise(self._lib.ermc_b200_session_solve(self.h, lo, hi, C.c_void_p(d_q),
                                                  C.c_void_p(d_sd), _ptr(steps, C.c_int64),
                                                  C.c_void_p(stream), buf, len(buf)), buf)
+        return steps
+
+    def solve_scatter(self, lo: int, hi: int, q_full: Sequence[int], sd_full: Sequence[int],
+                      stream: int = 0) -> np.ndarray:
+        """Solve [lo, hi) and store each cell's result into every buffer of
+        q_full / sd_full (device pointers: this GPU's and IPC-mapped peers')."""
+        steps = np.zeros(self.n_levels, dtype=np.int64)
+        n = len(q_full)
+        qa = (C.c_void_p * n)(*q_full)
+        sa = (C.c_void_p * n)(*sd_full)
+        buf = _err()
+        _raise(self._lib.ermc_b200_session_solve_scatter(
+            self.h, lo, hi, qa, sa, n, _ptr(steps, C.c_int64), C.c_void_p(stream), buf,
+            len(buf)), buf)
         return steps
 
     def timings(self) -> tuple[list[float], int]:

@@ -43,6 +43,8 @@ cudaError_t launch_trace_rays_fp64(const TraceParams& P, int64_t n,
                                    const int64_t* cells, const uint32_t* rays,
                                    const double* dirs, RayRecord* out,
                                    int64_t* level_steps, cudaStream_t s);
+cudaError_t launch_reduce_cells_scatter(const double* q_ray, int64_t n_cells, int rays,
+                                        const ScatterOut& out, int64_t base, cudaStream_t s);
 cudaError_t launch_reduce_cells(const double* q_ray, int64_t n_cells, int rays,
                                 double* q_r, double* std_dev, cudaStream_t s);
 cudaError_t launch_restrict(const double* fine, int fnx, int fny, int fnz,
@@ -765,8 +767,11 @@ void ensure_fp64_brick(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
 }
 
 // Core solve of [lo, hi) into device outputs.
+// scatter: write each cell's result into these full-field buffers at its
+// global index instead of d_q / d_sd (the fused all-gather).
 void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
-                        double* d_sd, int64_t* steps_out, cudaStream_t st) {
+                        double* d_sd, int64_t* steps_out, cudaStream_t st,
+                        const ermc_dev::ScatterOut* scatter = nullptr) {
   if (!s->field_set) throw Error("ermc_b200: temperature field not set");
   if (lo < 0 || hi > s->n_cells || lo > hi)
     throw Error("ermc_b200: cell range outside the grid");
@@ -863,8 +868,9 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
                "trace");
     cudaEventRecord(tt[ch].b, st);
     cudaEventRecord(tr[ch].a, st);
-    cuda_check(ermc_dev::launch_reduce_cells(s->d_qray.p, nc, R, d_q + (c0 - lo),
-                                             d_sd + (c0 - lo), st),
+    cuda_check(scatter ? ermc_dev::launch_reduce_cells_scatter(s->d_qray.p, nc, R, *scatter, c0, st)
+                       : ermc_dev::launch_reduce_cells(s->d_qray.p, nc, R, d_q + (c0 - lo),
+                                                       d_sd + (c0 - lo), st),
                "reduce");
     cudaEventRecord(tr[ch].b, st);
     s->launches += 2;
@@ -1196,6 +1202,62 @@ int ermc_b200_session_solve(ermc_session_t* s, int64_t cell_lo,
     session_solve_impl(s, cell_lo, cell_hi, d_q_r, d_std_dev, steps_per_level,
                        static_cast<cudaStream_t>(stream));
   });
+}
+
+int ermc_b200_session_solve_scatter(ermc_session_t* s, int64_t cell_lo, int64_t cell_hi,
+                                    double* const* d_q_full, double* const* d_sd_full,
+                                    int32_t n_out, int64_t* steps_per_level, void* stream,
+                                    char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    if (!s || !steps_per_level || !d_q_full || !d_sd_full) throw Error("ermc_b200: null argument");
+    if (n_out < 1 || n_out > ermc_dev::kMaxScatter)
+      throw Error("ermc_b200: n_out must be in [1, " + std::to_string(ermc_dev::kMaxScatter) + "]");
+    ermc_dev::ScatterOut out{};
+    out.n = n_out;
+    for (int p = 0; p < n_out; ++p) {
+      if (!d_q_full[p] || !d_sd_full[p]) throw Error("ermc_b200: null output buffer");
+      out.q[p] = d_q_full[p];
+      out.sd[p] = d_sd_full[p];
+    }
+    std::lock_guard<std::mutex> lk(s->mu);
+    session_solve_impl(s, cell_lo, cell_hi, nullptr, nullptr, steps_per_level,
+                       static_cast<cudaStream_t>(stream), &out);
+  });
+}
+
+int ermc_b200_device_alloc(int device, size_t bytes, void** d_ptr, char* errbuf,
+                           size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    if (!d_ptr) throw Error("ermc_b200: null argument");
+    DeviceGuard g(device);
+    cuda_check(cudaMalloc(d_ptr, std::max<size_t>(bytes, 1)), "cudaMalloc");
+  });
+}
+
+int ermc_b200_device_free(void* d_ptr) {
+  return cudaFree(d_ptr) == cudaSuccess ? 0 : 1;
+}
+
+int ermc_b200_ipc_export(const void* d_ptr, uint8_t handle[64], char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)), "cudaIpcGetMemHandle");
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+int ermc_b200_ipc_open(const uint8_t handle[64], void** d_ptr, char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    cuda_check(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle");
+  });
+}
+
+int ermc_b200_ipc_close(void* d_ptr) {
+  return cudaIpcCloseMemHandle(d_ptr) == cudaSuccess ? 0 : 1;
 }
 
 int ermc_b200_session_timings(const ermc_session_t* s, double* ms4,

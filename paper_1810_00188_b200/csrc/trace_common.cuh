@@ -106,6 +106,14 @@ struct TraceParams {
   int32_t* err_code;
 };
 
+// Full-field output buffers of the fused reduce + all-gather (K2 scatter).
+constexpr int kMaxScatter = 8;
+struct ScatterOut {
+  double* q[kMaxScatter];
+  double* sd[kMaxScatter];
+  int32_t n;
+};
+
 // Debug / test record of one traced ray (ermc_ray_result_t mirror).
 struct RayRecord {
   double q;

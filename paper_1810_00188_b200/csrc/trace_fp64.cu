@@ -1172,12 +1172,10 @@ __global__ void trace_rays_fp64(const __grid_constant__ TraceParams P,
 }
 
 // K2: per-cell tally in ray-id order (reference solver.cpp:142-155).
-__global__ void reduce_cells(const double* __restrict__ q_ray, int64_t n_cells,
-                             int rays, double* __restrict__ q_r,
-                             double* __restrict__ std_dev) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (c >= n_cells) return;
-  double sum = 0.0, mean = 0.0, m2 = 0.0;
+__device__ __forceinline__ void tally_cell(const double* __restrict__ q_ray, int64_t n_cells,
+                                           int rays, int64_t c, double& sum, double& sd) {
+  double mean = 0.0, m2 = 0.0;
+  sum = 0.0;
   for (int r = 0; r < rays; ++r) {
     const double x = q_ray[static_cast<int64_t>(r) * n_cells + c];
     sum += x;
@@ -1185,8 +1183,34 @@ __global__ void reduce_cells(const double* __restrict__ q_ray, int64_t n_cells,
     mean += delta / (r + 1);
     m2 += delta * (x - mean);
   }
+  sd = rays > 1 ? sqrt(m2 * rays / (rays - 1.0)) : 0.0;
+}
+
+__global__ void reduce_cells(const double* __restrict__ q_ray, int64_t n_cells,
+                             int rays, double* __restrict__ q_r,
+                             double* __restrict__ std_dev) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= n_cells) return;
+  double sum, sd;
+  tally_cell(q_ray, n_cells, rays, c, sum, sd);
   q_r[c] = sum;
-  std_dev[c] = rays > 1 ? sqrt(m2 * rays / (rays - 1.0)) : 0.0;
+  std_dev[c] = sd;
+}
+
+// K2 with the all-gather fused in: each cell's (Q_r, sigma) is stored into
+// every listed full-field buffer — this GPU's and its peers' (CUDA IPC
+// mappings; NVLink stores on a B200 node) — at its global index `base + c`,
+// so no collective follows the solve.
+__global__ void reduce_cells_scatter(const double* __restrict__ q_ray, int64_t n_cells,
+                                     int rays, ScatterOut out, int64_t base) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= n_cells) return;
+  double sum, sd;
+  tally_cell(q_ray, n_cells, rays, c, sum, sd);
+  for (int p = 0; p < out.n; ++p) {
+    out.q[p][base + c] = sum;
+    out.sd[p][base + c] = sd;
+  }
 }
 
 // K3: block-mean restriction (reference geometry.cpp:51-82), one thread per
@@ -1378,6 +1402,16 @@ cudaError_t launch_trace_rays_fp64(const TraceParams& P, int64_t n,
   const int64_t grid = (n + block - 1) / block;
   trace_rays_fp64<<<static_cast<unsigned>(grid), block, 0, stream>>>(
       P, n, cells, ray_ids, dirs, out, level_steps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_cells_scatter(const double* q_ray, int64_t n_cells, int rays,
+                                        const ScatterOut& out, int64_t base,
+                                        cudaStream_t stream) {
+  if (n_cells <= 0) return cudaSuccess;
+  const int block = 256;
+  reduce_cells_scatter<<<static_cast<unsigned>((n_cells + block - 1) / block), block, 0,
+                         stream>>>(q_ray, n_cells, rays, out, base);
   return cudaGetLastError();
 }
 
