@@ -13,6 +13,8 @@ kernel, ray-cell steps/s, steps per ray, and the check that applies:
   c4  config 4: 256^3 non-grey channel (the bench workload), fp64 and fp32;
   c5  config 5: rays-per-cell sweep at 256^3 — max / median sigma and time
       vs R, with log-log slopes (expected -0.5 and ~1);
+  full  a whole 128^3 config-3 field against the reference's solve() (every
+      cell, every step count);
   mg  multigrid ray coarsening (n_levels 1..7) on the config-4 field.
 Channel runs are checked per cell against the reference CPU solver
 (oracle/_ref, cell-subset replay — bitwise its solve() for those cells) on
@@ -137,7 +139,7 @@ def channel(out, name, n, model, tau, prec, rays, k_cells, fp64_ref=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.jsonl"))
-    ap.add_argument("--only", default="c1,c2,c3,c4,c5,mg")
+    ap.add_argument("--only", default="c1,c2,c3,full,c4,c5,mg")
     ap.add_argument("--cells", type=int, default=20000)
     a = ap.parse_args()
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
@@ -154,6 +156,19 @@ def main():
                           "fp64", 64, a.cells // 4)
             channel(a.out, f"c3 non-grey channel 128^3 {nb}x16", 128, f"nongrey{nb}", 1.0,
                     "fp32", 64, 0, fp64_ref=ref)
+    if "full" in which:
+        # Whole-field parity: a config-3 solve (128^3, 16 x 16, R = 64) against
+        # the reference's own solve() of the same field on all host threads.
+        g, t, b, m, _ = W.channel_case(128, "nongrey16")
+        cfg = capi.config_struct(rays_per_cell=64, seed=2024, workers=os.cpu_count() or 1)
+        q, sd, steps, ms, tms = device_solve(g, t, b, m, cfg)
+        rq, rsd, rsteps, rtotal, rwall = refshim.solve(g, t, b, m, cfg)
+        rep = fp64_report(q, rq, sd, rsd)
+        rep.update(cpu_total_steps=rtotal, cpu_wall_s=rwall, cpu_steps_per_s=rtotal / rwall,
+                   cpu_threads=os.cpu_count(), gpu_total_steps=int(np.sum(steps)),
+                   steps_equal=bool(int(np.sum(steps)) == rtotal))
+        record(a.out, **base("full-field c3 128^3 16x16 vs reference solve()", g, cfg, steps, ms,
+                             tms, "fp64"), full_field_parity=rep)
     if "c4" in which:
         ref = channel(a.out, "c4 non-grey channel 256^3 16x16", 256, "nongrey16", 1.0, "fp64",
                       64, a.cells)

@@ -18,6 +18,13 @@ for d in rows:
         chk = (f"vs reference CPU on {c['cells']} cells: {100 * c['frac_within_tol']:.2f} % within "
                f"1e-9 rel, max rel {c['max_rel']:.1e}, all within 3σ: {c['all_within_3sigma']}; "
                f"CPU {c['cpu_steps_per_s']:.3g} steps/s ({c['cpu_threads']} thr)")
+    if "full_field_parity" in d:
+        c = d["full_field_parity"]
+        chk = (f"every cell vs reference solve(): {100 * c['frac_within_tol']:.4f} % within 1e-9 "
+               f"rel, {c['bitwise_cells']} of {c['n']} bitwise, max rel {c['max_rel']:.1e}, "
+               f"all within 3σ: {c['all_within_3sigma']}, total steps equal: {c['steps_equal']}; "
+               f"CPU {c['cpu_steps_per_s']:.3g} steps/s ({c['cpu_threads']} thr, "
+               f"{c['cpu_wall_s']:.1f} s)")
     if "vs_fp64_same_rays" in d:
         c = d["vs_fp64_same_rays"]
         chk = (f"vs fp64 (same rays): {c['violations_3sigma']} cells outside 3σ "
