@@ -163,6 +163,19 @@ int ermc_b200_session_solve(ermc_session_t* s, int64_t cell_lo,
                             int64_t* steps_per_level, void* stream,
                             char* errbuf, size_t errlen);
 
+/* Asynchronous session_solve (the DNS coupling of PAPER.md:354,553: the host
+ * keeps computing while the radiation solve runs). session_solve_async
+ * validates the field and computes T_max (a short host wait for one device
+ * reduction), enqueues the sort, trace and reduction on `stream` and returns;
+ * session_wait blocks until they are done, then reports the step counts or
+ * the error the solve raised, exactly as session_solve would. One solve may
+ * be pending per session; wait before destroying the session or its stream. */
+int ermc_b200_session_solve_async(ermc_session_t* s, int64_t cell_lo,
+                                  int64_t cell_hi, double* d_q_r, double* d_std_dev,
+                                  void* stream, char* errbuf, size_t errlen);
+int ermc_b200_session_wait(ermc_session_t* s, int64_t* steps_per_level,
+                           char* errbuf, size_t errlen);
+
 /* session_solve with the all-gather fused into the per-cell reduction: each
  * cell's Q_r / sigma is stored into all n_out (<= 8) full-field buffers —
  * this device's and peer GPUs' (mapped with ermc_b200_ipc_open) — at its

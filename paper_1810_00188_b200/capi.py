@@ -88,6 +88,11 @@ EXPORTS = {
                                           C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
                                           C.c_char_p, C.c_size_t]),
     "ermc_b200_session_timings": (C.c_int, [C.c_void_p, _d, C.POINTER(C.c_int32)]),
+    "ermc_b200_session_solve_async": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                                C.c_void_p, C.c_void_p, C.c_char_p,
+                                                C.c_size_t]),
+    "ermc_b200_session_wait": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.c_char_p,
+                                         C.c_size_t]),
     "ermc_b200_session_solve_scatter": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64,
                                                   C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                                   C.c_int32, C.POINTER(C.c_int64), C.c_void_p,
@@ -368,6 +373,21 @@ class Session:
         _raise(self._lib.ermc_b200_session_solve(self.h, lo, hi, C.c_void_p(d_q),
                                                  C.c_void_p(d_sd), _ptr(steps, C.c_int64),
                                                  C.c_void_p(stream), buf, len(buf)), buf)
+        return steps
+
+    def solve_async(self, lo: int, hi: int, d_q: int, d_sd: int, stream: int = 0) -> None:
+        """Enqueue the solve of [lo, hi) on `stream` and return; see wait()."""
+        buf = _err()
+        _raise(self._lib.ermc_b200_session_solve_async(self.h, lo, hi, C.c_void_p(d_q),
+                                                       C.c_void_p(d_sd), C.c_void_p(stream),
+                                                       buf, len(buf)), buf)
+
+    def wait(self) -> np.ndarray:
+        """Block until the pending solve is done; its per-level step counts."""
+        steps = np.zeros(self.n_levels, dtype=np.int64)
+        buf = _err()
+        _raise(self._lib.ermc_b200_session_wait(self.h, _ptr(steps, C.c_int64), buf, len(buf)),
+               buf)
         return steps
 
     def solve_scatter(self, lo: int, hi: int, q_full: Sequence[int], sd_full: Sequence[int],

@@ -360,6 +360,19 @@ struct ermc_session {
   bool levels_valid = false;  // coarse levels match the current field
 
   double ms[4] = {0, 0, 0, 0};
+  // A solve enqueued but not yet waited for (session_solve_async): its
+  // stream, events, chunking, parameters (to describe a failing ray) and the
+  // pinned host words its counters are copied into.
+  struct Pending {
+    bool active = false;
+    cudaStream_t st = nullptr;
+    int64_t lo = 0, chunk_cells = 0, n_chunks = 0;
+    int rays = 0;
+    ermc_dev::TraceParams P{};
+    std::vector<Timing> tt, tr, ts;
+  } pending;
+  unsigned long long* h_words = nullptr;  // pinned: counters, codes, steps
+  size_t h_words_n = 0;
   int32_t launches = 0;
   std::mutex mu;
   size_t qray_budget_bytes = 0;
@@ -367,6 +380,11 @@ struct ermc_session {
   // wait for it before the buffers return to the pool.
   cudaEvent_t last_work = nullptr;
   ~ermc_session() {
+    if (pending.active) {  // never waited for: finish the work before the
+      DeviceGuard g(device);  // buffers go back to the pool
+      cudaStreamSynchronize(pending.st);
+    }
+    if (h_words) cudaFreeHost(h_words);
     if (last_work) {
       DeviceGuard g(device);
       cudaEventSynchronize(last_work);
@@ -769,9 +787,10 @@ void ensure_fp64_brick(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
 // Core solve of [lo, hi) into device outputs.
 // scatter: write each cell's result into these full-field buffers at its
 // global index instead of d_q / d_sd (the fused all-gather).
-void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
-                        double* d_sd, int64_t* steps_out, cudaStream_t st,
-                        const ermc_dev::ScatterOut* scatter = nullptr) {
+void session_enqueue(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
+                     double* d_sd, cudaStream_t st,
+                     const ermc_dev::ScatterOut* scatter = nullptr) {
+  if (s->pending.active) throw Error("ermc_b200: a solve is pending on this session; wait first");
   if (!s->field_set) throw Error("ermc_b200: temperature field not set");
   if (lo < 0 || hi > s->n_cells || lo > hi)
     throw Error("ermc_b200: cell range outside the grid");
@@ -875,50 +894,94 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
     cudaEventRecord(tr[ch].b, st);
     s->launches += 2;
   }
-  std::vector<unsigned long long> counters(2 * std::max<int64_t>(n_chunks, 1));
-  std::vector<int32_t> codes(std::max<int64_t>(n_chunks, 1));
-  unsigned long long steps[ermc_dev::kMaxLevels];
-  cuda_check(cudaMemcpyAsync(counters.data(), s->d_counters.p,
-                             counters.size() * sizeof(unsigned long long),
+  // Counters, error codes and step counts into pinned host words (so the
+  // copies stay asynchronous); session_finish reads them after the stream.
+  const size_t n_cnt = 2 * static_cast<size_t>(std::max<int64_t>(n_chunks, 1));
+  const size_t n_codes = static_cast<size_t>(std::max<int64_t>(n_chunks, 1));
+  const size_t need = n_cnt + n_codes + ermc_dev::kMaxLevels;
+  if (s->h_words_n < need) {
+    if (s->h_words) cudaFreeHost(s->h_words);
+    s->h_words = nullptr;
+    cuda_check(cudaMallocHost(&s->h_words, need * sizeof(unsigned long long)), "cudaMallocHost");
+    s->h_words_n = need;
+  }
+  cuda_check(cudaMemcpyAsync(s->h_words, s->d_counters.p, n_cnt * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, st),
              "D2H");
-  cuda_check(cudaMemcpyAsync(codes.data(), s->d_errcode.p, codes.size() * sizeof(int32_t),
+  cuda_check(cudaMemcpyAsync(s->h_words + n_cnt, s->d_errcode.p, n_codes * sizeof(int32_t),
                              cudaMemcpyDeviceToHost, st),
              "D2H");
-  cuda_check(cudaMemcpyAsync(steps, s->d_steps.p, sizeof(steps), cudaMemcpyDeviceToHost, st),
+  cuda_check(cudaMemcpyAsync(s->h_words + n_cnt + n_codes, s->d_steps.p,
+                             ermc_dev::kMaxLevels * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st),
              "D2H");
+  auto& pd = s->pending;
+  pd.active = true;
+  pd.st = st;
+  pd.lo = lo;
+  pd.chunk_cells = chunk_cells;
+  pd.n_chunks = n_chunks;
+  pd.rays = R;
+  pd.P = P;
+  pd.tt = std::move(tt);
+  pd.tr = std::move(tr);
+  pd.ts = std::move(ts);
+}
+
+// Waits for the enqueued solve: kernel times, the error word (a failing ray
+// is re-traced by the debug kernel for the reference's message), step counts.
+void session_finish(ermc_session* s, int64_t* steps_out) {
+  auto& pd = s->pending;
+  if (!pd.active) throw Error("ermc_b200: no solve pending on this session");
+  pd.active = false;
+  DeviceGuard guard(s->device);
+  cudaStream_t st = pd.st;
   cuda_check(cudaStreamSynchronize(st), "trace sync");
+  const int64_t n_chunks = pd.n_chunks;
+  const size_t n_cnt = 2 * static_cast<size_t>(std::max<int64_t>(n_chunks, 1));
+  const size_t n_codes = static_cast<size_t>(std::max<int64_t>(n_chunks, 1));
+  const unsigned long long* counters = s->h_words;
+  const unsigned long long* steps = s->h_words + n_cnt + n_codes;
   for (int64_t ch = 0; ch < n_chunks; ++ch) {
     float a = 0.f, b = 0.f;
-    cudaEventElapsedTime(&a, tt[ch].a, tt[ch].b);
-    cudaEventElapsedTime(&b, tr[ch].a, tr[ch].b);
+    cudaEventElapsedTime(&a, pd.tt[ch].a, pd.tt[ch].b);
+    cudaEventElapsedTime(&b, pd.tr[ch].a, pd.tr[ch].b);
     s->ms[2] += a;
     s->ms[3] += b;
-    if (ts[ch].a) {
+    if (pd.ts[ch].a) {
       float c = 0.f;
-      cudaEventElapsedTime(&c, ts[ch].a, ts[ch].b);
+      cudaEventElapsedTime(&c, pd.ts[ch].a, pd.ts[ch].b);
       s->ms[1] += c;
-      cudaEventDestroy(ts[ch].a);
-      cudaEventDestroy(ts[ch].b);
+      cudaEventDestroy(pd.ts[ch].a);
+      cudaEventDestroy(pd.ts[ch].b);
     }
-    cudaEventDestroy(tt[ch].a);
-    cudaEventDestroy(tt[ch].b);
-    cudaEventDestroy(tr[ch].a);
-    cudaEventDestroy(tr[ch].b);
+    cudaEventDestroy(pd.tt[ch].a);
+    cudaEventDestroy(pd.tt[ch].b);
+    cudaEventDestroy(pd.tr[ch].a);
+    cudaEventDestroy(pd.tr[ch].b);
   }
+  const int R = pd.rays;
   for (int64_t ch = 0; ch < n_chunks; ++ch) {
     const unsigned long long key = counters[2 * ch + 1];
     if (key == 0ull) continue;
-    const int64_t c0 = lo + ch * chunk_cells;
+    const int64_t c0 = pd.lo + ch * pd.chunk_cells;
     const uint64_t w = key - 1;
     const int64_t cell = c0 + static_cast<int64_t>(w / R);
     const uint32_t ray = static_cast<uint32_t>(w % R);
     // Describe with the fp64 debug tracer (reference arithmetic).
+    ermc_dev::TraceParams P = pd.P;
     P.lv[0].field = s->d_field.p;
     throw Error(describe_failure(s, P, cell, ray, st));
   }
   for (int l = 0; l < s->config.n_levels; ++l)
     steps_out[l] = static_cast<int64_t>(steps[l]);
+}
+
+void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
+                        double* d_sd, int64_t* steps_out, cudaStream_t st,
+                        const ermc_dev::ScatterOut* scatter = nullptr) {
+  session_enqueue(s, lo, hi, d_q, d_sd, st, scatter);
+  session_finish(s, steps_out);
 }
 
 void set_field_impl(ermc_session* s, const double* t, int is_device,
@@ -1258,6 +1321,25 @@ int ermc_b200_ipc_open(const uint8_t handle[64], void** d_ptr, char* errbuf, siz
 
 int ermc_b200_ipc_close(void* d_ptr) {
   return cudaIpcCloseMemHandle(d_ptr) == cudaSuccess ? 0 : 1;
+}
+
+int ermc_b200_session_solve_async(ermc_session_t* s, int64_t cell_lo, int64_t cell_hi,
+                                  double* d_q_r, double* d_std_dev, void* stream,
+                                  char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    if (!s) throw Error("ermc_b200: null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
+    session_enqueue(s, cell_lo, cell_hi, d_q_r, d_std_dev, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ermc_b200_session_wait(ermc_session_t* s, int64_t* steps_per_level, char* errbuf,
+                           size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    if (!s || !steps_per_level) throw Error("ermc_b200: null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
+    session_finish(s, steps_per_level);
+  });
 }
 
 int ermc_b200_session_timings(const ermc_session_t* s, double* ms4,

@@ -303,3 +303,34 @@ def test_dispatch_order_never_changes_results(precision):
                         {"ERMC_SORT": "1", "ERMC_SORT_BLOCK": "8"},  # cubic tiles, clipped
                         {"ERMC_SORT": "1", "ERMC_SORT_BLOCK": "4"})]
     assert all(r == runs[0] for r in runs[1:])
+
+
+def test_async_session_overlaps_the_host_and_matches_sync():
+    # session_solve_async returns while the solve runs (the host can advance a
+    # DNS step meanwhile); wait() then gives the same bytes and
+    # step counts as the synchronous call, and errors surface at wait().
+    import time
+    import torch
+    g, t, b, m = W.channel_case(64, "nongrey16")[:4]
+    n = g.nx * g.ny * g.nz
+    cfg = capi.config_struct(rays_per_cell=32, seed=5)
+    s = capi.Session(g, b, m, cfg)
+    td = torch.from_numpy(t).cuda()
+    s.set_field(td.data_ptr(), True, 0)
+    q1 = torch.empty(n, dtype=torch.float64, device="cuda")
+    sd1 = torch.empty_like(q1)
+    st1 = s.solve(0, n, q1.data_ptr(), sd1.data_ptr(), 0)
+    t_sync = s.timings()[0][2]
+    q2 = torch.empty_like(q1)
+    sd2 = torch.empty_like(q1)
+    t0 = time.perf_counter()
+    s.solve_async(0, n, q2.data_ptr(), sd2.data_ptr(), 0)
+    enqueue_ms = (time.perf_counter() - t0) * 1e3
+    with pytest.raises(capi.ErmcError, match="pending"):
+        s.solve_async(0, n, q2.data_ptr(), sd2.data_ptr(), 0)
+    st2 = s.wait()
+    with pytest.raises(capi.ErmcError, match="no solve pending"):
+        s.wait()
+    assert torch.equal(q1, q2) and torch.equal(sd1, sd2) and list(st1) == list(st2)
+    assert enqueue_ms < 0.5 * t_sync, (enqueue_ms, t_sync)
+    s.close()
