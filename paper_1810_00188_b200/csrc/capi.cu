@@ -60,7 +60,7 @@ cudaError_t launch_build_iv32(const double* k, const double* ib, int nb,
 cudaError_t launch_to_fp32(const double* src, float* dst, int64_t n,
                            cudaStream_t s);
 cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny,
-                                   int nz, cudaStream_t s);
+                                   int nz, int b, cudaStream_t s);
 cudaError_t launch_to_bricked64(const double* src, double* dst, int nx, int ny, int nz,
                                 cudaStream_t s);
 int sort_max_bins();
@@ -343,6 +343,7 @@ struct ermc_session {
   std::vector<ermc_grid_t> level_grids;
   DevBuf<float> d_field32;
   DevBuf<float> d_field32b;
+  int fp32_brick_edge = 0;  // layout of d_field32b (2 or 4)
   DevBuf<double> d_field64b;
   std::vector<std::unique_ptr<DevBuf<float>>> d_levels32;
   DevBuf<float4> d_iv32;
@@ -1031,13 +1032,22 @@ void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
   }
   P.lv[0].field32 = s->d_field32.p;
   const ermc_grid_t& g0 = s->grid;
-  const bool even = g0.nx % 2 == 0 && g0.ny % 2 == 0 && g0.nz % 2 == 0;
-  P.brick = (tune().brick && even && s->config.n_levels == 1) ? 1 : 0;
+  // brick edge: ERMC_BRICK=4 asks for 4^3 bricks (dimensions divisible by 4),
+  // otherwise 2^3 bricks on even grids
+  auto divisible = [&](int b) { return g0.nx % b == 0 && g0.ny % b == 0 && g0.nz % b == 0; };
+  int edge = 0;
+  if (tune().brick && s->config.n_levels == 1) {
+    if (tune().brick == 4 && divisible(4) && !P.track_pos) edge = 4;
+    else if (divisible(2)) edge = 2;
+  }
+  if (s->fp32_brick_edge != edge) s->d_field32b.reset();  // layout changed
+  s->fp32_brick_edge = edge;
+  P.brick = edge;
   if (P.brick) {
     if (!s->d_field32b.p) {
       s->d_field32b.ensure(static_cast<size_t>(s->n_cells));
       cuda_check(ermc_dev::launch_to_fp32_bricked(s->d_field.p, s->d_field32b.p, g0.nx,
-                                                  g0.ny, g0.nz, st),
+                                                  g0.ny, g0.nz, edge, st),
                  "to_fp32_bricked");
       ++s->launches;
     }

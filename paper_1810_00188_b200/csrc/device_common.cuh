@@ -105,6 +105,14 @@ __device__ __forceinline__ int brick_index(const LevelDesc& L, int i, int j, int
          ((j & 1) << 1) + (k & 1);
 }
 
+// The same for kB^3 bricks (kB = 2 or 4; grid dimensions divisible by kB).
+template <int kB>
+__device__ __forceinline__ int brick_index_b(const LevelDesc& L, int i, int j, int k) {
+  const int nby = L.n[1] / kB, nbz = L.n[2] / kB;
+  return (((i / kB) * nby + (j / kB)) * nbz + (k / kB)) * (kB * kB * kB) +
+         ((i % kB) * kB + (j % kB)) * kB + (k % kB);
+}
+
 // std::upper_bound over a short ascending array (sampling.cpp:44-51).
 __device__ __forceinline__ int upper_bound_d(const double* a, int n, double x) {
   int first = 0, count = n;

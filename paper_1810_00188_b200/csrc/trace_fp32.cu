@@ -574,7 +574,8 @@ struct Fp32Lean {
 // kPos = false when every wall is black: a wall hit ends the ray, so the
 // position (p0) and direction are dead after setup and periodic re-basing
 // only shifts the ray parameter (frees 6 registers; see Fp64Lean).
-template <int kHint, bool kPos = true>
+// kB: brick edge (2: 2x2x2 bricks = one 32-byte sector; 4: 4x4x4 = 256 B).
+template <int kHint, bool kPos = true, int kB = 2>
 struct Fp32Brick {
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
@@ -599,9 +600,10 @@ struct Fp32Brick {
   }
 
   __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx) {
-    const int nby = (L.n[1] + 1) >> 1, nbz = (L.n[2] + 1) >> 1;
+    constexpr int kV = kB * kB * kB;
+    const int nby = L.n[1] / kB, nbz = L.n[2] / kB;
     const int bs[3] = {nby * nbz, nbz, 1};
-    const int sn[3] = {4, 2, 1};
+    const int sn[3] = {kB * kB, kB, 1};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const float da = dir[a];
@@ -617,12 +619,12 @@ struct Fp32Brick {
           static_cast<float>(L.origin[a] + (idx[a] + (up ? 1 : 0)) * L.d[a]);
       tn[a] = (face - p0[a]) * inv;
       const float td = static_cast<float>(L.d[a]) * fabsf(inv);
-      const int far = up ? 8 * bs[a] - sn[a] : sn[a] - 8 * bs[a];
+      const int far = up ? kV * bs[a] - (kB - 1) * sn[a] : (kB - 1) * sn[a] - kV * bs[a];
       axr[a * kBlock32] = make_int2(__float_as_int(td), far);
       axl[a * kBlock32] = up ? L.n[a] - 1 - idx[a] : idx[a];
     }
     s = 0.0f;
-    lin = brick_index(L, idx[0], idx[1], idx[2]);
+    lin = brick_index_b<kB>(L, idx[0], idx[1], idx[2]);
   }
 
   __device__ __forceinline__ void rebase() {
@@ -696,7 +698,9 @@ struct Fp32Brick {
     const int left = left0 - 1;
     const bool inside = left >= 0;
     const bool periodic = (P.periodic_mask >> axis) & 1;
-    int nlin = lin + ((left0 & 1) ? (far > 0 ? (4 >> axis) : -(4 >> axis)) : far);
+    // the step leaves its brick when the cells-left counter is a multiple of kB
+    const int near = kB == 2 ? (4 >> axis) : (16 >> (2 * axis));
+    int nlin = lin + ((left0 & (kB - 1)) ? (far > 0 ? near : -near) : far);
     float t_next = t_cur;
     if (inside) {
       t_next = ld_t32<kHint>(L.field32b + nlin);
@@ -705,7 +709,7 @@ struct Fp32Brick {
 #pragma unroll
       for (int a = 0; a < 3; ++a)
         idx[a] = a == axis ? (far > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
-      nlin = brick_index(L, idx[0], idx[1], idx[2]);
+      nlin = brick_index_b<kB>(L, idx[0], idx[1], idx[2]);
       t_next = ld_t32<kHint>(L.field32b + nlin);
     }
 
@@ -797,26 +801,26 @@ struct Fp32Brick {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-template <int kMinBlocks, int kHint, bool kPos = true>
+template <int kMinBlocks, int kHint, bool kPos = true, int kB = 2>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
   stage_cdfs32(P);
-  pool_kernel_body<Fp32Brick<kHint, kPos>, false>(P);
+  pool_kernel_body<Fp32Brick<kHint, kPos, kB>, false>(P);
 }
 
-// Converts the fp64 k-fastest field to the fp32 micro-brick layout.
+// Converts the fp64 k-fastest field to the fp32 micro-brick layout (edge b).
 __global__ void to_fp32_bricked(const double* __restrict__ src, float* __restrict__ dst,
-                                int nx, int ny, int nz) {
+                                int nx, int ny, int nz, int b) {
   const int64_t n = static_cast<int64_t>(nx) * ny * nz;
-  const int nby = (ny + 1) >> 1, nbz = (nz + 1) >> 1;
+  const int nby = ny / b, nbz = nz / b;
   for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < n;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int i = static_cast<int>(c / (static_cast<int64_t>(ny) * nz));
     const int j = static_cast<int>((c / nz) % ny);
     const int k = static_cast<int>(c % nz);
-    const int64_t b = ((static_cast<int64_t>(i >> 1) * nby + (j >> 1)) * nbz + (k >> 1)) * 8 +
-                      ((i & 1) << 2) + ((j & 1) << 1) + (k & 1);
-    dst[b] = static_cast<float>(src[c]);
+    const int64_t idx = ((static_cast<int64_t>(i / b) * nby + (j / b)) * nbz + (k / b)) * (b * b * b) +
+                        ((i % b) * b + (j % b)) * b + (k % b);
+    dst[idx] = static_cast<float>(src[c]);
   }
 }
 
@@ -896,6 +900,7 @@ TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
     return eight ? trace_pool_fp32_lean_mg<8> : trace_pool_fp32_lean_mg<6>;
   }
   if (fp32_lean(P) && P.brick) {
+    if (!P.track_pos && P.brick == 4) return trace_pool_fp32_brick<8, 0, false, 4>;
     if (!P.track_pos)
       return eight ? trace_pool_fp32_brick<8, 0, false> : trace_pool_fp32_brick<6, 0, false>;
     return eight ? trace_pool_fp32_brick<8, 0> : trace_pool_fp32_brick<6, 0>;
@@ -928,8 +933,8 @@ cudaError_t launch_build_iv32(const double* k, const double* ib, int nb, int nq,
 }
 
 cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny,
-                                   int nz, cudaStream_t stream) {
-  to_fp32_bricked<<<1184, 256, 0, stream>>>(src, dst, nx, ny, nz);
+                                   int nz, int b, cudaStream_t stream) {
+  to_fp32_bricked<<<1184, 256, 0, stream>>>(src, dst, nx, ny, nz, b);
   return cudaGetLastError();
 }
 

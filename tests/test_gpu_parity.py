@@ -334,3 +334,27 @@ def test_async_session_overlaps_the_host_and_matches_sync():
     assert torch.equal(q1, q2) and torch.equal(sd1, sd2) and list(st1) == list(st2)
     assert enqueue_ms < 0.5 * t_sync, (enqueue_ms, t_sync)
     s.close()
+
+
+def test_fp32_brick_layouts_give_identical_bytes():
+    # The fp32 field layout (2^3 or 4^3 micro-bricks) changes addressing only:
+    # the same rays, the same arithmetic, byte-identical Q_r / sigma / steps.
+    def run(env):
+        import json
+        import os
+        import subprocess
+        import sys
+        from pathlib import Path
+        root = Path(__file__).resolve().parent.parent
+        code = (
+            "import sys, json\n"
+            f"sys.path[:0] = [{str(root)!r}]\n"
+            "from paper_1810_00188_b200 import capi, workloads as W\n"
+            "g, t, b, m = W.channel_case(32, 'nongrey16')[:4]\n"
+            "q, sd, st, tot, _ = capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=16, "
+            "seed=3, precision=capi.FP32))\n"
+            "print(json.dumps([q.tobytes().hex(), sd.tobytes().hex(), int(tot)]))\n")
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
+                             capture_output=True, text=True, check=True).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    assert run({"ERMC_BRICK": "1"}) == run({"ERMC_BRICK": "4"})
