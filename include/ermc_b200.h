@@ -189,7 +189,8 @@ int ermc_b200_session_solve_scatter(ermc_session_t* s, int64_t cell_lo,
                                     char* errbuf, size_t errlen);
 
 /* Device buffers shareable across processes (cudaMalloc'd, so their CUDA IPC
- * handles address the buffer itself). */
+ * handles address the buffer itself). No reference counterpart: the
+ * reference solver is one process (solver.cpp:106-170). */
 int ermc_b200_device_alloc(int device, size_t bytes, void** d_ptr, char* errbuf,
                            size_t errlen);
 int ermc_b200_device_free(void* d_ptr);
