@@ -286,6 +286,7 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
       // Several march steps per pool check: amortises the ballots; a lane
       // whose ray ends early idles for < inner_steps iterations.
       int st = kContinue;
+#pragma unroll 2  // measured +0.2 % (fp64) / +0.6 % (fp32)
       for (int s = 0; s < P.inner_steps && st == kContinue; ++s)
         st = tr.step(P, max_steps);
       if (st != kContinue) {
