@@ -194,6 +194,44 @@ class DevicePool {
   std::unordered_map<void*, size_t> size_;
 };
 
+// Pinned host words for the solve's counters (so their copies stay
+// asynchronous). cudaMallocHost / cudaFreeHost are slow and the latter
+// synchronises the device, so blocks are recycled process-wide instead of
+// being allocated per session (one-shot solves create a session per call).
+class PinnedPool {
+ public:
+  static PinnedPool& get() {
+    static PinnedPool* pool = new PinnedPool();  // never destroyed
+    return *pool;
+  }
+  unsigned long long* alloc(size_t words, size_t* got) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (size_t i = 0; i < free_.size(); ++i)
+        if (free_[i].second >= words) {
+          auto b = free_[i];
+          free_.erase(free_.begin() + static_cast<long>(i));
+          *got = b.second;
+          return b.first;
+        }
+    }
+    const size_t n = std::max<size_t>(words, 4096);
+    void* p = nullptr;
+    cuda_check(cudaMallocHost(&p, n * sizeof(unsigned long long)), "cudaMallocHost");
+    *got = n;
+    return static_cast<unsigned long long*>(p);
+  }
+  void free(unsigned long long* p, size_t words) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu_);
+    free_.emplace_back(p, words);
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<unsigned long long*, size_t>> free_;
+};
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -385,7 +423,7 @@ struct ermc_session {
       DeviceGuard g(device);  // buffers go back to the pool
       cudaStreamSynchronize(pending.st);
     }
-    if (h_words) cudaFreeHost(h_words);
+    PinnedPool::get().free(h_words, h_words_n);
     if (last_work) {
       DeviceGuard g(device);
       cudaEventSynchronize(last_work);
@@ -901,10 +939,8 @@ void session_enqueue(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
   const size_t n_codes = static_cast<size_t>(std::max<int64_t>(n_chunks, 1));
   const size_t need = n_cnt + n_codes + ermc_dev::kMaxLevels;
   if (s->h_words_n < need) {
-    if (s->h_words) cudaFreeHost(s->h_words);
-    s->h_words = nullptr;
-    cuda_check(cudaMallocHost(&s->h_words, need * sizeof(unsigned long long)), "cudaMallocHost");
-    s->h_words_n = need;
+    PinnedPool::get().free(s->h_words, s->h_words_n);
+    s->h_words = PinnedPool::get().alloc(need, &s->h_words_n);
   }
   cuda_check(cudaMemcpyAsync(s->h_words, s->d_counters.p, n_cnt * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, st),
@@ -1127,6 +1163,10 @@ void solve_part(const ermc_grid_t* grid, const double* temperature,
   }
   cuda_check(cudaStreamSynchronize(st), "sync");
   mark("d2h q, sigma");
+  dq.reset();
+  dsd.reset();
+  s.reset();
+  mark("teardown");
 }
 
 // Host-buffer entry points (ermc_b200_solve / _solve_range): the range is
