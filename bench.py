@@ -193,7 +193,7 @@ def run_reference(a, world, rank):
     cfg = capi.config_struct(rays_per_cell=a.rays, seed=a.seed, workers=os.cpu_count() or 1)
     threads = os.cpu_count() or 1
     ref = CpuReference(grid, t, b, m, cfg, threads)
-    ref.size(max(5.0, min(a.cpu_seconds, 20.0)))
+    ref.size(max(2.0, min(a.cpu_seconds, 6.0)))  # ~5 s per step: K + W steps stay within minutes
     vals = []
     last = None
     for i in range(a.warmup + a.steps):
