@@ -317,6 +317,8 @@ struct Timing {
 struct Tune {
   int inner_steps = 32;    // fp64 march steps per pool check
   int inner_steps32 = 48;  // fp32
+  int inner_steps_mg = 48;    // multigrid (n_levels > 1), fp64: measured -1..-4 % time
+  int inner_steps32_mg = 64;  // multigrid, fp32: measured -1 %
   int refill = 8;
   int fp64_min_blocks = 0;  // 0 = per-tracer default (trace_fp64.cu)
   int fp32_min_blocks = 8;
@@ -340,6 +342,8 @@ const Tune& tune() {
     Tune x;
     x.inner_steps = std::max(1, env_int("ERMC_INNER_STEPS", x.inner_steps));
     x.inner_steps32 = std::max(1, env_int("ERMC_INNER_STEPS32", x.inner_steps32));
+    x.inner_steps_mg = std::max(1, env_int("ERMC_INNER_STEPS_MG", x.inner_steps_mg));
+    x.inner_steps32_mg = std::max(1, env_int("ERMC_INNER_STEPS32_MG", x.inner_steps32_mg));
     x.refill = std::max(1, std::min(32, env_int("ERMC_REFILL", x.refill)));
     x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
@@ -728,7 +732,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.h_seed = mix64_host(c.seed + 0x9e3779b97f4a7c15ULL);
   P.rays = c.rays_per_cell;
   P.refill_threshold = tune().refill;
-  P.inner_steps = tune().inner_steps;
+  P.inner_steps = c.n_levels > 1 ? tune().inner_steps_mg : tune().inner_steps;
   P.lean = tune().lean;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
@@ -845,7 +849,7 @@ void session_enqueue(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
   ermc_dev::TraceParams& P = pr.P;
   const bool fp32 = s->config.precision == ERMC_PRECISION_FP32;
   if (fp32) {
-    P.inner_steps = tune().inner_steps32;
+    P.inner_steps = P.n_levels > 1 ? tune().inner_steps32_mg : tune().inner_steps32;
     ensure_fp32_inputs(s, P, st);
   }
   else

@@ -140,6 +140,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.jsonl"))
     ap.add_argument("--only", default="c1,c2,c3,full,c4,c5,mg")
+    ap.add_argument("--mg-levels", default="1,2,3,4,5,6,7")
+    ap.add_argument("--mg-precisions", default="fp64,fp32")
+    ap.add_argument("--no-cpu-check", action="store_true",
+                    help="skip the multigrid CPU parity samples (timing A/Bs)")
     ap.add_argument("--cells", type=int, default=20000)
     a = ap.parse_args()
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
@@ -195,14 +199,14 @@ def main():
                    time_slope=float(np.polyfit(lr, np.log([x[3] for x in rows]), 1)[0]))
     if "mg" in which:
         g, t, b, m, _ = W.channel_case(256, "nongrey16")
-        for prec in ("fp64", "fp32"):
-            for lv in (1, 2, 3, 4, 5, 6, 7):
+        for prec in a.mg_precisions.split(","):
+            for lv in (int(x) for x in a.mg_levels.split(",")):
                 cfg = capi.config_struct(rays_per_cell=64, seed=2024, n_levels=lv,
                                          steps_per_level=5, coarsen_ratio=2,
                                          precision=capi.FP64 if prec == "fp64" else capi.FP32)
                 q, sd, steps, ms, tms = device_solve(g, t, b, m, cfg)
                 rep = {}
-                if prec == "fp64" and lv > 1:
+                if prec == "fp64" and lv > 1 and not a.no_cpu_check:
                     rep["cpu_parity"] = cpu_check(g, t, b, m, cfg, q, sd, a.cells // 4)
                 record(a.out, **base(f"mg multigrid 256^3 levels={lv}", g, cfg, steps, ms, tms,
                                      prec),
