@@ -230,6 +230,7 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
   uint32_t pool_next = 0, pool_end = 0;
   bool exhausted = false;
   unsigned long long my_steps = 0;
+  uint32_t lvl_steps = 0;  // kMulti: lane l accumulates level l (l < n_levels)
 
   while (true) {
     const unsigned idle = __ballot_sync(kFullMask, !active);
@@ -282,13 +283,22 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
     if (__ballot_sync(kFullMask, active) == 0u && exhausted &&
         pool_next >= pool_end)
       break;
+    int done_lvl = -1;  // kMulti: final level of a ray that just ended
+    uint32_t done_sal = 0;
     if (active) {
       // Several march steps per pool check: amortises the ballots; a lane
       // whose ray ends early idles for < inner_steps iterations.
       int st = kContinue;
+      if constexpr (kMulti) {
+        // not unrolled: the demotion makes the step body large (i-cache)
+#pragma unroll 1
+        for (int s = 0; s < P.inner_steps && st == kContinue; ++s)
+          st = tr.step(P, max_steps);
+      } else {
 #pragma unroll 2  // measured +0.2 % (fp64) / +0.6 % (fp32)
-      for (int s = 0; s < P.inner_steps && st == kContinue; ++s)
-        st = tr.step(P, max_steps);
+        for (int s = 0; s < P.inner_steps && st == kContinue; ++s)
+          st = tr.step(P, max_steps);
+      }
       if (st != kContinue) {
         active = false;
         if (st == kDone) {
@@ -299,11 +309,8 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
             // streaming store: keep the L2 for the temperature field
             __stcs(P.q_ray + static_cast<uint64_t>(ray) * P.n_cells + cell, q);
             if (kMulti) {
-              for (int l = 0; l < tr.level(); ++l)
-                atomicAdd(&s_steps[l],
-                          static_cast<unsigned long long>(P.lv[l].cap));
-              atomicAdd(&s_steps[tr.level()],
-                        static_cast<unsigned long long>(tr.sal()));
+              done_lvl = tr.level();
+              done_sal = static_cast<uint32_t>(tr.sal());
             } else {
               my_steps += static_cast<unsigned long long>(tr.steps());
             }
@@ -315,12 +322,37 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         }
       }
     }
+    // Per-level step counts of the rays that just ended: a ray that ended on
+    // level L took cap_l steps on every level l < L and sal on L. Summed per
+    // warp here (converged) instead of one shared-memory 64-bit atomic per
+    // ray and level — those compile to CAS loops that, contended by every
+    // warp of the block, took ~20 % of the multigrid kernel's time.
+    if (kMulti && __any_sync(kFullMask, done_lvl >= 0)) {
+      for (int l = 0; l < P.n_levels; ++l) {
+        const uint32_t c = done_lvl > l    ? static_cast<uint32_t>(P.lv[l].cap)
+                           : done_lvl == l ? done_sal
+                                           : 0u;
+        const uint32_t lo = __reduce_add_sync(kFullMask, c & 0xffffu);
+        const uint32_t hi = __reduce_add_sync(kFullMask, c >> 16);
+        if (lane == static_cast<unsigned>(l)) {
+          const unsigned long long add = lo + (static_cast<unsigned long long>(hi) << 16);
+          if (lvl_steps + add >= 0x80000000ull) {  // keep the register 32-bit
+            atomicAdd(&s_steps[l], lvl_steps + add);
+            lvl_steps = 0;
+          } else {
+            lvl_steps += static_cast<uint32_t>(add);
+          }
+        }
+      }
+    }
   }
   if (!kMulti) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
       my_steps += __shfl_xor_sync(kFullMask, my_steps, o);
     if (lane == 0) atomicAdd(&s_steps[0], my_steps);
+  } else if (lane < static_cast<unsigned>(P.n_levels) && lvl_steps != 0u) {
+    atomicAdd(&s_steps[lane], static_cast<unsigned long long>(lvl_steps));
   }
 }
 

@@ -3,6 +3,10 @@
 usage: python tools/ncu_summary.py <tag> <prof_fp64.ncu-rep> <prof_fp32.ncu-rep> <steps_fp64> <steps_fp32>
 Writes profiles/ncu_<tag>_{fp64,fp32}.csv (raw metrics of interest) and
 updates profiles/ncu_trace_summary.json (per-step DRAM traffic used by bench.py).
+
+       python tools/ncu_summary.py --one <out.csv> <prof.ncu-rep>
+Writes the metrics of one capture plus its warp-stall shares (per-instruction
+samples of the source page, summed) to <out.csv>.
 """
 import csv, json, subprocess, sys
 from pathlib import Path
@@ -49,7 +53,38 @@ def to_bytes(v):
     return float(val.replace(",", "")) * UNIT.get(unit, 1.0)
 
 
+def stall_shares(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr = rows[1]
+    cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    tot = {hdr[i]: 0 for i in cols}
+    for r in rows[2:]:
+        for i in cols:
+            tot[hdr[i]] += int(r[i] or 0)
+    n = sum(tot.values()) or 1
+    return {k: 100.0 * v / n for k, v in sorted(tot.items(), key=lambda x: -x[1])}, len(rows) - 2
+
+
+def one(out, rep):
+    name, m = metrics(rep)
+    shares, n_sass = stall_shares(rep)
+    with open(out, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["metric", "value", "unit"])
+        w.writerow(["kernel", name, ""])
+        w.writerow(["sass_instructions", n_sass, ""])
+        for k, (v, u) in m.items():
+            w.writerow([k, v, u])
+        for k, v in shares.items():
+            w.writerow([f"stall_share.{k}", f"{v:.2f}", "%"])
+
+
 def main():
+    if sys.argv[1] == "--one":
+        one(sys.argv[2], sys.argv[3])
+        return
     tag, r64, r32, s64, s32 = sys.argv[1:6]
     prof = Path("profiles")
     summary_path = prof / "ncu_trace_summary.json"
