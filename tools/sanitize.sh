@@ -17,10 +17,12 @@ for name, n, v in cases:
 g, t, b, m = W.channel_case(16, "nongrey16")[:4]
 for prec in (capi.FP64, capi.FP32):
     capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec, n_devices=2))
+    capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec, n_levels=4,
+                                              steps_per_level=2))  # black-wall multigrid tracers
 print("sanitizer cases done")
 PY
 sed -i "s#ROOT#$PWD#g" /tmp/san_case.py
 timeout 1500 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_memcheck.txt 2>&1; echo "memcheck rc=$?" >> $OUT/sanitize_memcheck.txt
 ERMC_SORT_BLOCK=8 timeout 1500 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_memcheck_blk.txt 2>&1; echo "memcheck rc=$?" >> $OUT/sanitize_memcheck_blk.txt
 timeout 1500 $CS --tool racecheck --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_racecheck.txt 2>&1; echo "racecheck rc=$?" >> $OUT/sanitize_racecheck.txt
-tail -3 $OUT/sanitize_memcheck.txt $OUT/sanitize_memcheck_blk.txt $OUT/sanitize_racecheck.txt
+tail -n 3 $OUT/sanitize_memcheck.txt $OUT/sanitize_memcheck_blk.txt $OUT/sanitize_racecheck.txt
