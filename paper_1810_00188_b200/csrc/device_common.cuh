@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "trace_common.cuh"
 
@@ -199,6 +200,15 @@ __device__ __forceinline__ void raise_error(const TraceParams& P, uint64_t key,
   if (old == 0ull || old > key + 1) atomicExch(P.err_code, code);
 }
 
+// Tracer::kWideLevelSteps (optional): the multigrid per-level step counter
+// is 64-bit instead of 32-bit (a register-allocation choice, measured per
+// tracer).
+template <class T, class = void>
+struct wide_level_steps : std::false_type {};
+template <class T>
+struct wide_level_steps<T, std::void_t<decltype(T::kWideLevelSteps)>>
+    : std::integral_constant<bool, T::kWideLevelSteps> {};
+
 // Persistent ray pool. Every lane owns one ray; when at least
 // refill_threshold lanes of a warp are idle they take the next work items
 // (positions in the dispatch order: P.perm, or cell-major (cell, ray) ids)
@@ -336,7 +346,9 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         const uint32_t hi = __reduce_add_sync(kFullMask, c >> 16);
         if (lane == static_cast<unsigned>(l)) {
           const unsigned long long add = lo + (static_cast<unsigned long long>(hi) << 16);
-          if (lvl_steps + add >= 0x80000000ull) {  // keep the register 32-bit
+          if (wide_level_steps<Tracer>::value) {
+            my_steps += add;
+          } else if (lvl_steps + add >= 0x80000000ull) {  // keep the register 32-bit
             atomicAdd(&s_steps[l], lvl_steps + add);
             lvl_steps = 0;
           } else {
@@ -351,8 +363,9 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
     for (int o = 16; o > 0; o >>= 1)
       my_steps += __shfl_xor_sync(kFullMask, my_steps, o);
     if (lane == 0) atomicAdd(&s_steps[0], my_steps);
-  } else if (lane < static_cast<unsigned>(P.n_levels) && lvl_steps != 0u) {
-    atomicAdd(&s_steps[lane], static_cast<unsigned long long>(lvl_steps));
+  } else {
+    const unsigned long long v = wide_level_steps<Tracer>::value ? my_steps : lvl_steps;
+    if (lane < static_cast<unsigned>(P.n_levels) && v != 0ull) atomicAdd(&s_steps[lane], v);
   }
 }
 

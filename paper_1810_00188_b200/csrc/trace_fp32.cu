@@ -342,6 +342,8 @@ struct Fp32Tracer {
 // kReflect = false (every wall black): no reflection code.
 template <int kHint, bool kMulti = false, bool kReflect = true>
 struct Fp32Lean {
+  // multigrid level counters in 64-bit registers: measured ~3 % faster here
+  static constexpr bool kWideLevelSteps = true;
   float p0[3], dir[3], tn[3];
   float s, tau, acc, ib1n, last_ib2n, t_cur;
   double cq;
