@@ -139,7 +139,7 @@ def channel(out, name, n, model, tau, prec, rays, k_cells, fp64_ref=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.jsonl"))
-    ap.add_argument("--only", default="c1,c2,c3,full,c4,c5,mg")
+    ap.add_argument("--only", default="c1,c2,c3,full,fullmg,c4,c5,mg")
     ap.add_argument("--mg-levels", default="1,2,3,4,5,6,7")
     ap.add_argument("--mg-precisions", default="fp64,fp32")
     ap.add_argument("--no-cpu-check", action="store_true",
@@ -173,6 +173,21 @@ def main():
                    steps_equal=bool(int(np.sum(steps)) == rtotal))
         record(a.out, **base("full-field c3 128^3 16x16 vs reference solve()", g, cfg, steps, ms,
                              tms, "fp64"), full_field_parity=rep)
+    if "fullmg" in which:
+        # The same whole-field check for multigrid ray coarsening (4 levels).
+        g, t, b, m, _ = W.channel_case(128, "nongrey16")
+        cfg = capi.config_struct(rays_per_cell=64, seed=2024, workers=os.cpu_count() or 1,
+                                 n_levels=4, steps_per_level=5, coarsen_ratio=2)
+        q, sd, steps, ms, tms = device_solve(g, t, b, m, cfg)
+        rq, rsd, rsteps, rtotal, rwall = refshim.solve(g, t, b, m, cfg)
+        rep = fp64_report(q, rq, sd, rsd)
+        rep.update(cpu_total_steps=rtotal, cpu_wall_s=rwall, cpu_steps_per_s=rtotal / rwall,
+                   cpu_threads=os.cpu_count(), gpu_total_steps=int(np.sum(steps)),
+                   steps_equal=bool(int(np.sum(steps)) == rtotal),
+                   steps_per_level_equal=bool([int(x) for x in steps] == [int(x) for x in rsteps]))
+        record(a.out, **base("full-field c3 128^3 16x16, 4-level multigrid, vs reference solve()",
+                             g, cfg, steps, ms, tms, "fp64"),
+               steps_per_level=[int(x) for x in steps], full_field_parity=rep)
     if "c4" in which:
         ref = channel(a.out, "c4 non-grey channel 256^3 16x16", 256, "nongrey16", 1.0, "fp64",
                       64, a.cells)
