@@ -269,6 +269,15 @@ int ermc_b200_abi_version(void);
  * has no device memory). Returns 0. */
 int ermc_b200_release_cached_memory(int device);
 
+/* L2 bandwidth probe (measurement only; no reference counterpart): reads
+ * an L2-resident buffer of `bytes` (1 MiB .. ~64 MiB) on `device` (-1 =
+ * current). mode 0: streaming 16-byte ld.global.cg sweeps, `iters` times;
+ * mode 1: independent hashed 8-byte gathers, one 32-byte sector each,
+ * counted as sector bytes. *gbs = bytes moved / kernel time (CUDA events).
+ * The denominator of bench.py's roofline.l2. */
+int ermc_b200_probe_l2(int device, size_t bytes, int iters, int mode, double* gbs,
+                       char* errbuf, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

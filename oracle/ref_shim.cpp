@@ -127,12 +127,15 @@ int ref_solve(const ermc_grid_t* grid, const double* temperature,
 // build_cdfs / planck_mean / build_hierarchy / init_ray / march API:
 // bitwise identical to solve() for the selected cells.
 // steps_per_level receives the per-level sum over the selected cells.
-int ref_solve_cells(const ermc_grid_t* grid, const double* temperature,
-                    const ermc_boundary_t* boundary, const ermc_model_t* model,
-                    const ermc_config_t* config, int64_t n_sel,
-                    const int64_t* cells, double* q_r, double* std_dev,
-                    int64_t* steps_per_level, int32_t n_threads,
-                    double* wall_time, char* errbuf, size_t errlen) {
+// cell_steps (nullable) receives each selected cell's march steps summed
+// over its rays and levels.
+int ref_solve_cells_ex(const ermc_grid_t* grid, const double* temperature,
+                       const ermc_boundary_t* boundary, const ermc_model_t* model,
+                       const ermc_config_t* config, int64_t n_sel,
+                       const int64_t* cells, double* q_r, double* std_dev,
+                       int64_t* steps_per_level, int64_t* cell_steps,
+                       int32_t n_threads, double* wall_time, char* errbuf,
+                       size_t errlen) {
   try {
     auto t0 = std::chrono::steady_clock::now();
     ermc::CartesianGrid g = to_grid(grid);
@@ -153,6 +156,7 @@ int ref_solve_cells(const ermc_grid_t* grid, const double* temperature,
         g, field.values, cfg.n_levels, cfg.coarsen_ratio, cfg.steps_per_level);
     ermc::TraceOptions opt{cfg.tolerance, cfg.max_steps, cfg.specular_walls};
     int nt = std::max(1, n_threads);
+    if (cell_steps) std::fill(cell_steps, cell_steps + n_sel, int64_t{0});
     std::vector<std::vector<int64_t>> steps(nt, std::vector<int64_t>(cfg.n_levels, 0));
     std::vector<std::string> errors(nt);
     auto work = [&](int w) {
@@ -171,6 +175,7 @@ int ref_solve_cells(const ermc_grid_t* grid, const double* temperature,
             per_ray[r] = res.q_contribution;
             for (int l = 0; l < cfg.n_levels; ++l)
               steps[w][l] += res.steps_per_level[l];
+            if (cell_steps) cell_steps[s] += res.steps;
           }
           double sum = 0.0, mean = 0.0, m2 = 0.0;
           for (int r = 0; r < n_rays; ++r) {
@@ -208,6 +213,17 @@ int ref_solve_cells(const ermc_grid_t* grid, const double* temperature,
     put_err(errbuf, errlen, e.what());
     return 1;
   }
+}
+
+int ref_solve_cells(const ermc_grid_t* grid, const double* temperature,
+                    const ermc_boundary_t* boundary, const ermc_model_t* model,
+                    const ermc_config_t* config, int64_t n_sel,
+                    const int64_t* cells, double* q_r, double* std_dev,
+                    int64_t* steps_per_level, int32_t n_threads,
+                    double* wall_time, char* errbuf, size_t errlen) {
+  return ref_solve_cells_ex(grid, temperature, boundary, model, config, n_sel,
+                            cells, q_r, std_dev, steps_per_level, nullptr,
+                            n_threads, wall_time, errbuf, errlen);
 }
 
 int ref_trace_rays(const ermc_grid_t* grid, const double* temperature,

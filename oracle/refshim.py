@@ -50,6 +50,12 @@ def lib() -> C.CDLL:
                                       C.POINTER(Model), C.POINTER(Config), C.c_int64,
                                       C.POINTER(C.c_int64), _d, _d, C.POINTER(C.c_int64),
                                       C.c_int32, _d, C.c_char_p, C.c_size_t]
+        L.ref_solve_cells_ex.restype = C.c_int
+        L.ref_solve_cells_ex.argtypes = [C.POINTER(Grid), _d, C.POINTER(Boundary),
+                                         C.POINTER(Model), C.POINTER(Config), C.c_int64,
+                                         C.POINTER(C.c_int64), _d, _d, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int64), C.c_int32, _d, C.c_char_p,
+                                         C.c_size_t]
         L.ref_trace_rays.restype = C.c_int
         L.ref_trace_rays.argtypes = [C.POINTER(Grid), _d, C.POINTER(Boundary),
                                      C.POINTER(Model), C.POINTER(Config), C.c_double,
@@ -116,6 +122,25 @@ def solve_cells(grid, temperature, boundary, model, config, cells, threads=None)
                                  _p(cells, C.c_int64), _p(q), _p(sd), _p(steps, C.c_int64),
                                  nt, C.byref(wall), buf, len(buf)), buf)
     return q, sd, steps, wall.value
+
+
+def solve_cells_steps(grid, temperature, boundary, model, config, cells, threads=None):
+    """solve_cells plus each selected cell's march steps (summed over its
+    rays and levels). Returns (q, sd, steps_per_level, cell_steps, wall)."""
+    t = np.ascontiguousarray(temperature, dtype=np.float64).ravel()
+    cells = np.ascontiguousarray(cells, dtype=np.int64)
+    q, sd = np.zeros(len(cells)), np.zeros(len(cells))
+    steps = np.zeros(config.n_levels, dtype=np.int64)
+    cell_steps = np.zeros(len(cells), dtype=np.int64)
+    wall = C.c_double()
+    nt = threads or os.cpu_count() or 1
+    buf = C.create_string_buffer(2048)
+    _check(lib().ref_solve_cells_ex(C.byref(grid), _p(t), C.byref(boundary),
+                                    C.byref(model.desc), C.byref(config), len(cells),
+                                    _p(cells, C.c_int64), _p(q), _p(sd),
+                                    _p(steps, C.c_int64), _p(cell_steps, C.c_int64), nt,
+                                    C.byref(wall), buf, len(buf)), buf)
+    return q, sd, steps, cell_steps, wall.value
 
 
 def trace_rays(grid, temperature, boundary, model, config, t_max, qe, cells, rays,

@@ -37,6 +37,7 @@ CUDA_SOURCES = [
     ("trace_fp32.cu", []),
     ("dispatch.cu", []),
     ("capi.cu", []),
+    ("probe.cu", []),
 ]
 HOST_SOURCES = ["host_tables.cpp", "host_api.cpp", "host_io.cpp"]
 

@@ -119,6 +119,8 @@ EXPORTS = {
     "ermc_b200_device_count": (C.c_int, []),
     "ermc_b200_abi_version": (C.c_int, []),
     "ermc_b200_release_cached_memory": (C.c_int, [C.c_int]),
+    "ermc_b200_probe_l2": (C.c_int, [C.c_int, C.c_size_t, C.c_int, C.c_int, _d, C.c_char_p,
+                                     C.c_size_t]),
 }
 
 
@@ -331,6 +333,15 @@ def ipc_open(handle: bytes) -> int:
     buf = _err()
     _raise(lib.ermc_b200_ipc_open(h, C.byref(p), buf, len(buf)), buf)
     return p.value
+
+
+def probe_l2(device: int = 0, nbytes: int = 48 << 20, iters: int = 20, mode: int = 0) -> float:
+    """Measured L2 read bandwidth, GB/s (mode 0 streaming, 1 sector gather)."""
+    lib = load()
+    out = C.c_double()
+    buf = _err()
+    _raise(lib.ermc_b200_probe_l2(device, nbytes, iters, mode, C.byref(out), buf, len(buf)), buf)
+    return out.value
 
 
 def uniform_device(seed: int, cells, rays, draws) -> np.ndarray:

@@ -18,48 +18,13 @@ solver's own API so the CPU reference and the GPU consume identical bytes.
 """
 from __future__ import annotations
 
-import math
-import random
-
-import numpy as np
-
 from . import capi
-
-LX, LY, LZ = 4.0 * math.pi, 2.0, 2.0 * math.pi
-T_WALL_LO, T_WALL_HI = 955.0, 573.0
-
-
-def channel_modes(n_modes: int = 24, seed: int = 1234):
-    rng = random.Random(seed)
-    modes = []
-    for _ in range(n_modes):
-        kx = rng.randint(1, 6)
-        ky = rng.randint(1, 4)
-        kz = rng.randint(1, 6)
-        phi = rng.uniform(0.0, 2.0 * math.pi)
-        a = rng.gauss(0.0, 1.0)
-        modes.append((kx, ky, kz, phi, a))
-    return modes
+from .channel import (LX, LY, LZ, N_QUAD, T_WALL_HI, T_WALL_LO, TEMP_GRID,  # noqa: F401
+                      channel_field, channel_modes, spacing, stratified_runs)
 
 
 def channel_grid(n: int) -> capi.Grid:
-    return capi.make_grid((n, n, n), (LX / n, LY / n, LZ / n))
-
-
-def channel_field(n: int) -> np.ndarray:
-    """T at cell centres, k-fastest (i = x, j = y, k = z), float64."""
-    dx, dy, dz = LX / n, LY / n, LZ / n
-    x = (np.arange(n) + 0.5) * dx
-    y = (np.arange(n) + 0.5) * dy
-    z = (np.arange(n) + 0.5) * dz
-    pert = np.zeros((n, n, n))
-    for kx, ky, kz, phi, a in channel_modes():
-        cxz = np.cos(kx * x[:, None] / 2.0 + kz * z[None, :] + phi)  # (x, z)
-        sy = np.sin(ky * math.pi * y / 2.0)                          # (y,)
-        pert += a * cxz[:, None, :] * sy[None, :, None]
-    t = (955.0 - 191.0 * y)[None, :, None] + \
-        (40.0 / math.sqrt(24.0)) * np.sin(math.pi * y / 2.0)[None, :, None] * pert
-    return np.ascontiguousarray(t.reshape(-1))
+    return capi.make_grid((n, n, n), spacing(n))
 
 
 def channel_boundary(wall_eps: float = 1.0) -> capi.Boundary:
@@ -87,6 +52,28 @@ def nongrey_channel_model(n_bands: int = 16, n_quad: int = 16, strength: float =
     return E.build_k_distribution(sp, E.make_bands(sp.nu_grid[0], sp.nu_grid[-1] + 1e-6,
                                                    n_bands),
                                   E.QuadratureSet.gauss_legendre(n_quad))
+
+
+def file_hashes(n: int, t, model_obj) -> dict:
+    """FNV-1a hashes (reference io.cpp:374-389) of the workload's TFLD1 field
+    and KTAB1 tables as written by this package's own writers; bench.py's
+    reference arm writes the same files with the reference's writers and
+    reports the same keys, so equal configs mean byte-identical inputs."""
+    import os  # noqa: PLC0415
+    import tempfile  # noqa: PLC0415
+
+    E = _ermc()
+    g = E.CartesianGrid()
+    g.nx = g.ny = g.nz = n
+    g.dx, g.dy, g.dz = spacing(n)
+    f = E.TemperatureField()
+    f.grid = g
+    f.values = t.tolist()
+    with tempfile.TemporaryDirectory() as d:
+        E.write_tfld(os.path.join(d, "t.tfld"), f)
+        E.write_ktab(os.path.join(d, "m.ktab"), model_obj)
+        return {"tfld_fnv": E.file_hash(os.path.join(d, "t.tfld")),
+                "ktab_fnv": E.file_hash(os.path.join(d, "m.ktab"))}
 
 
 def channel_case(n: int, model: str = "nongrey16", tau: float = 1.0, wall_eps: float = 1.0):
