@@ -419,6 +419,7 @@ struct ermc_session {
   int32_t launches = 0;
   std::mutex mu;
   size_t qray_budget_bytes = 0;
+  bool tables_finite = true;  // every k / Ib table entry finite (lean tracers allowed)
   // Marks the last asynchronous work (set_field's copy) so the destructor can
   // wait for it before the buffers return to the pool.
   cudaEvent_t last_work = nullptr;
@@ -458,6 +459,11 @@ void copy_model(ermc_session* s, const ermc_model_t& m) {
   s->model.k_table = s->k.data();
   s->model.ib_table = s->ib.data();
   s->view = ermc_host::make_view_unchecked(s->model);
+  // The lean tracers drop interp's frac == 0 shortcut (a + 0 * (b - a) == a
+  // only for finite b): with any non-finite table entry the solve runs the
+  // reference-order tracers, which keep it (spectral.cpp:179-205).
+  s->tables_finite = std::all_of(s->k.begin(), s->k.end(), [](double x) { return std::isfinite(x); }) &&
+                     std::all_of(s->ib.begin(), s->ib.end(), [](double x) { return std::isfinite(x); });
 }
 
 ermc_session* create_session(const ermc_grid_t* grid,
@@ -490,6 +496,11 @@ ermc_session* create_session(const ermc_grid_t* grid,
   size_t free_b = 0, total_b = 0;
   cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   s->qray_budget_bytes = std::min<size_t>(free_b / 4, size_t(16) << 30);
+  // Test hook: a small per-ray buffer budget forces many chunks (bytes).
+  if (const char* e = std::getenv("ERMC_QRAY_BUDGET")) {
+    const long long v = std::atoll(e);
+    if (v > 0) s->qray_budget_bytes = static_cast<size_t>(v);
+  }
 
   cudaStream_t st = nullptr;
   s->d_temps.upload(s->temps.data(), s->temps.size(), st);
@@ -733,7 +744,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.rays = c.rays_per_cell;
   P.refill_threshold = tune().refill;
   P.inner_steps = c.n_levels > 1 ? tune().inner_steps_mg : tune().inner_steps;
-  P.lean = tune().lean;
+  P.lean = tune().lean && s->tables_finite;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;
@@ -840,6 +851,8 @@ void session_enqueue(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
   for (double& m : s->ms) m = 0.0;
   s->launches = 0;
   DeviceGuard guard(s->device);
+  // set_field may have copied on another stream: order the solve after it.
+  if (s->last_work) cuda_check(cudaStreamWaitEvent(st, s->last_work, 0), "stream wait");
   const double t_max = validate_field_and_tmax(s, st);
   Prepared pr;
   // build_cdfs (inside prepare) may throw before the hierarchy checks, as
@@ -1027,6 +1040,10 @@ void session_solve_impl(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
 
 void set_field_impl(ermc_session* s, const double* t, int is_device,
                     cudaStream_t st) {
+  // The pending solve reads d_field and the derived fp32 / brick copies that
+  // this call overwrites and frees.
+  if (s->pending.active)
+    throw Error("ermc_b200: a solve is pending on this session; wait before set_field");
   DeviceGuard guard(s->device);
   s->d_field.ensure(static_cast<size_t>(s->n_cells));
   cuda_check(cudaMemcpyAsync(s->d_field.p, t, s->n_cells * sizeof(double),
@@ -1052,6 +1069,8 @@ void ensure_fp32_inputs(ermc_session* s, ermc_dev::TraceParams& P,
   if (v.nt < 2 || !v.uniform)
     throw Error("ermc_b200: the fp32 kernel needs a uniform temperature grid "
                 "with at least 2 nodes; use precision=fp64");
+  if (!s->tables_finite)
+    throw Error("ermc_b200: the fp32 kernel needs finite k / Ib tables; use precision=fp64");
   for (const ermc_grid_t& g : s->level_grids)
     if (cells_of(g) >= (int64_t(1) << 31))
       throw Error("ermc_b200: the fp32 kernel supports grids below 2^31 "
