@@ -63,6 +63,8 @@ cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny
                                    int nz, int b, cudaStream_t s);
 cudaError_t launch_to_bricked64(const double* src, double* dst, int nx, int ny, int nz,
                                 cudaStream_t s);
+cudaError_t launch_build_cell_words(const TraceParams& P, const double* field, int64_t n,
+                                    double scale, uint64_t* out, int* bad, cudaStream_t s);
 int sort_max_bins();
 int sort_max_tile_items();
 cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_rows,
@@ -332,6 +334,7 @@ struct Tune {
   int sort_tile_items = 1 << 16;
   int sort_block = 0;  // cubic sort tiles (edge in cells; 0 = linear tiles)
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
+  int cellw = 1;       // fp64 lean tracers read precomputed cell words (trace_fp64.cu)
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -357,6 +360,7 @@ const Tune& tune() {
     x.sort_tile_items = std::max(1, env_int("ERMC_SORT_TILE", x.sort_tile_items));
     x.sort_dirs = std::max(1, env_int("ERMC_SORT_DIRS", x.sort_dirs));
     x.sort_block = std::max(0, env_int("ERMC_SORT_BLOCK", x.sort_block));
+    x.cellw = env_int("ERMC_CELLW", x.cellw);
     return x;
   }();
   return t;
@@ -387,6 +391,10 @@ struct ermc_session {
   DevBuf<float> d_field32b;
   int fp32_brick_edge = 0;  // layout of d_field32b (2 or 4)
   DevBuf<double> d_field64b;
+  // cell words of every level (fp64 lean tracers); valid until set_field
+  std::vector<std::unique_ptr<DevBuf<uint64_t>>> d_cellw;
+  DevBuf<int> d_cw_bad;
+  bool cellw_valid = false, cellw_ok = false;
   std::vector<std::unique_ptr<DevBuf<float>>> d_levels32;
   DevBuf<float4> d_iv32;
   bool iv32_ready = false;
@@ -838,6 +846,63 @@ void ensure_fp64_brick(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
   P.lv[0].field64b = s->d_field64b.p;
 }
 
+// fp64 lean tracers: cell words of every level (trace_fp64.cu decode_cw), built
+// once per field. They need an exactly arithmetic temperature grid (the
+// kernel's dt), at most 256 intervals, and every in-range T - t[lo] to be an
+// integer multiple of 2^-s below 2^53 * 2^-s with s = 52 - floor(log2 t_first);
+// the builder checks every cell and the solve keeps the temperature-reading
+// tracers if one does not fit.
+void ensure_cell_words(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t st) {
+  const ermc_host::TableView& v = s->view;
+  P.cellw = 0;
+  if (!tune().cellw || !P.lean || P.brick || !P.tint_arith || v.nt < 2 || v.nt - 1 > 256 ||
+      !(v.temps[0] > 0.0))
+    return;
+  int e = 0;
+  std::frexp(v.temps[0], &e);              // t_first = f 2^e, f in [0.5, 1)
+  const double scale = std::ldexp(1.0, 52 - (e - 1));  // 1 / ulp(t_first)
+  const double cw_dt = v.dt * scale;
+  if (!(cw_dt < 9007199254740992.0)) return;  // m must convert exactly
+  P.cw_shift = 56;
+  P.cw_dt = cw_dt;
+  P.cw_rdt = 1.0 / cw_dt;
+  if (!s->cellw_valid) {
+    Timing t;
+    cudaEventCreate(&t.a);
+    cudaEventCreate(&t.b);
+    cudaEventRecord(t.a, st);
+    const size_t nl = s->level_grids.size();
+    s->d_cellw.resize(nl);
+    s->d_cw_bad.ensure(1);
+    cuda_check(cudaMemsetAsync(s->d_cw_bad.p, 0, sizeof(int), st), "memset");
+    for (size_t l = 0; l < nl; ++l) {
+      if (!s->d_cellw[l]) s->d_cellw[l] = std::make_unique<DevBuf<uint64_t>>();
+      const int64_t n = cells_of(s->level_grids[l]);
+      s->d_cellw[l]->ensure(static_cast<size_t>(n));
+      const double* field = l == 0 ? s->d_field.p : s->d_levels[l]->p;
+      cuda_check(ermc_dev::launch_build_cell_words(P, field, n, scale, s->d_cellw[l]->p,
+                                                   s->d_cw_bad.p, st),
+                 "build_cell_words");
+      ++s->launches;
+    }
+    cudaEventRecord(t.b, st);
+    int bad = 0;
+    cuda_check(cudaMemcpyAsync(&bad, s->d_cw_bad.p, sizeof(int), cudaMemcpyDeviceToHost, st),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(st), "cell words");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    s->ms[0] += ms;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+    s->cellw_valid = true;
+    s->cellw_ok = bad == 0;
+  }
+  if (!s->cellw_ok) return;
+  for (size_t l = 0; l < s->d_cellw.size(); ++l) P.lv[l].cellw = s->d_cellw[l]->p;
+  P.cellw = 1;
+}
+
 // Core solve of [lo, hi) into device outputs.
 // scatter: write each cell's result into these full-field buffers at its
 // global index instead of d_q / d_sd (the fused all-gather).
@@ -865,8 +930,10 @@ void session_enqueue(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
     P.inner_steps = P.n_levels > 1 ? tune().inner_steps32_mg : tune().inner_steps32;
     ensure_fp32_inputs(s, P, st);
   }
-  else
+  else {
     ensure_fp64_brick(s, P, st);
+    ensure_cell_words(s, P, st);
+  }
 
   const int R = s->config.rays_per_cell;
   const int64_t total_cells = hi - lo;
@@ -1058,6 +1125,7 @@ void set_field_impl(ermc_session* s, const double* t, int is_device,
   s->levels_valid = false;
   s->iv32_ready = s->iv32_ready;  // tables unchanged
   s->d_levels32.clear();
+  s->cellw_valid = false;
   s->d_field32.reset();
   s->d_field32b.reset();
   s->d_field64b.reset();

@@ -28,6 +28,10 @@ struct LevelDesc {
   const float* field32;  // fp32 copy for the fast kernel (may be null)
   const float* field32b;   // fp32 in 2x2x2 micro-bricks (even grids, lean kernel)
   const double* field64b;  // fp64 in 2x2x2 micro-bricks (even grids, lean kernel)
+  // Table coordinates of every cell (lean fp64 tracers, see TraceParams::cw_*):
+  // (lo << cw_shift) | m, where lo is the reference lookup's interval and
+  // m * 2^-cw_scale_exp == T - t[lo] exactly.
+  const uint64_t* cellw;
 };
 
 // Error codes raised on the device; the host re-traces the failing ray
@@ -70,6 +74,13 @@ struct TraceParams {
   int32_t tint_arith;        // every node is exactly l*dt + t0 and every width
                              // exactly dt, so tint[l] is computed, not loaded
   double t_first, t_last;    // table range
+  // Cell words (LevelDesc::cellw): the lookup's (lo, frac) precomputed per
+  // cell once per field. frac = RN(m / cw_dt) with cw_dt = dt * 2^s and
+  // cw_rdt = RN(1 / cw_dt) (Markstein: the reference's RN((T - t[lo]) / dt),
+  // bitwise; the builder checks it cell by cell).
+  int32_t cellw;             // 1: the lean fp64 tracers read cell words
+  int32_t cw_shift;          // lo = w >> cw_shift (64 - bits of the interval index)
+  double cw_dt, cw_rdt;
 
   // ---- fp32 fast-path tables (trace_fp32.cu) ----
   const float4* iv32;        // [n_bands*n_quad][n_temps-1] {k_lo, k_hi-k_lo, ib_lo, ib_hi-ib_lo}

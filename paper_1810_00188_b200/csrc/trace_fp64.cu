@@ -411,13 +411,29 @@ __device__ __forceinline__ bool lookup_spec(const TraceParams& P, const double4*
   return true;
 }
 
+// Cell words (TraceParams::cw_*): the lookup of a cell's temperature,
+// precomputed once per field. The interval index sits in the top 8 bits;
+// the low 56 hold m = (T - t[lo]) * 2^s, an exact integer because every
+// in-range T and table node is a multiple of ulp(t_first) = 2^-s, and
+// T - t[lo] is exact (Sterbenz: t[lo] <= T <= t[lo] + dt <= 2 t[lo]).
+// frac = RN(m / (dt 2^s)) = RN((T - t[lo]) / dt), the reference's quotient
+// (spectral.cpp:148-177) — the builder verifies it for every cell.
+constexpr int kCwShift = 56;
+
+__device__ __forceinline__ void decode_cw(const TraceParams& P, uint64_t w, int& lo,
+                                          double& frac) {
+  lo = static_cast<int>(w >> kCwShift);
+  const uint64_t m = w & ((1ull << kCwShift) - 1ull);
+  frac = div_rcp(static_cast<double>(m), P.cw_dt, P.cw_rdt);
+}
+
 // init_ray (reference sampling.cpp:55-96) for global cell `cell`, with the
 // level-0 grid. Returns an error code (0 = ok).
 // cdf: the staged sampling CDFs (lean kernels) or null for P's global copy.
 // kLean: the lean tracers' variant — the table lookup runs on the packed
 // interval records (lookup_spec: same values), and the DDA setup is left to
 // the tracer, which builds its own per-axis records.
-template <bool kLean = false>
+template <bool kLean = false, bool kCW = false>
 __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
                                         uint32_t ray_id, Ray& r,
                                         const double* dir_override,
@@ -471,19 +487,22 @@ __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
       r.pos[a] += (draw_u(r.h_cell, ray_id, r.next_draw++) - 0.5) * L.d[a];
   }
 
-  double t_cell = __ldg(L.field + cell);
   int lo;
   double frac;
   double k1;
   if (kLean) {
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}: copies of the table values
-    if (!lookup_spec<0>(P, P.iv64 + (n * P.n_quad + g) * (P.n_temps - 1), t_cell, lo, frac,
-                        v))
+    const double4* row = P.iv64 + (n * P.n_quad + g) * (P.n_temps - 1);
+    if (kCW) {
+      decode_cw(P, __ldg(L.cellw + cell), lo, frac);
+      v = ld_rec64<0>(row + lo);
+    } else if (!lookup_spec<0>(P, row, __ldg(L.field + cell), lo, frac, v)) {
       return kErrTableRange;
+    }
     r.ib1 = frac == 0.0 ? v.z : v.z + frac * (v.w - v.z);
     k1 = frac == 0.0 ? v.x : v.x + frac * (v.y - v.x);
   } else {
-    if (!t_lookup(P, t_cell, lo, frac)) return kErrTableRange;
+    if (!t_lookup(P, __ldg(L.field + cell), lo, frac)) return kErrTableRange;
     r.ib1 = interp_row(r.ibrow, lo, frac);
     k1 = interp_row(r.krow, lo, frac);
   }
@@ -755,11 +774,18 @@ constexpr int kLeanRecs64 = 4;
 
 // kReflect = false (every wall black) drops the reflection code; the
 // multigrid tracer keeps positions for demotion but can still drop it.
-template <int kHint, bool kBrick, bool kPos = true, bool kMulti = false, bool kReflect = kPos>
+// kCW: the cells are read as cell words (LevelDesc::cellw: the lookup's
+// interval and exact offset, precomputed per field) instead of temperatures,
+// so a step decodes (lo, frac) with one shift, one mask, one conversion and
+// one Markstein quotient instead of running the table lookup.
+template <int kHint, bool kBrick, bool kPos = true, bool kMulti = false, bool kReflect = kPos,
+          bool kCW = false>
 struct Fp64Lean {
   static_assert(!kMulti || (kPos && !kBrick), "demotion reads positions, k-fastest levels");
+  static_assert(!kCW || !kBrick, "cell words use the k-fastest layout");
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
+  uint64_t w_cur;  // kCW: the current cell's word
   int4* ax;
   int row;  // first interval record of (band, g) in iv64
   int lin, steps_;
@@ -809,7 +835,7 @@ struct Fp64Lean {
     Ray r;
     const double* cdf =
         P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock) : nullptr;
-    const int e = init_ray<true>(P, cell, ray, r, nullptr, cdf);
+    const int e = init_ray<true, kCW>(P, cell, ray, r, nullptr, cdf);
     if (e != kErrNone) return e;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -828,7 +854,10 @@ struct Fp64Lean {
     sal_ = 0;
     ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
                                static_cast<int>(cell), static_cast<int>(ray));
-    t_cur = __ldg(P.lv[0].field + cell);
+    if (kCW)
+      w_cur = __ldg(P.lv[0].cellw + cell);
+    else
+      t_cur = __ldg(P.lv[0].field + cell);
     setup(P.lv[0], r.idx);
     return kErrNone;
   }
@@ -857,7 +886,10 @@ struct Fp64Lean {
     }
     sal_ = 0;
     setup(C, idx);
-    t_cur = __ldg(C.field + lin);
+    if (kCW)
+      w_cur = __ldg(C.cellw + lin);
+    else
+      t_cur = __ldg(C.field + lin);
     return kErrNone;
   }
 
@@ -878,7 +910,10 @@ struct Fp64Lean {
     int lo;
     double frac;
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
-    if (!lookup_spec<kHint>(P, P.iv64 + row, t_cur, lo, frac, v)) {
+    if (kCW) {
+      decode_cw(P, w_cur, lo, frac);
+      v = ld_rec64<kHint>(P.iv64 + row + lo);
+    } else if (!lookup_spec<kHint>(P, P.iv64 + row, t_cur, lo, frac, v)) {
       err = kErrTableRange;
       return kFail;
     }
@@ -916,8 +951,13 @@ struct Fp64Lean {
       if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
     }
     double t_next = t_cur;
-    if (inside || periodic)
-      t_next = ld_t64<kHint>((kBrick ? L.field64b : L.field) + nlin);
+    uint64_t w_next = w_cur;
+    if (inside || periodic) {
+      if (kCW)
+        w_next = __ldg(L.cellw + nlin);
+      else
+        t_next = ld_t64<kHint>((kBrick ? L.field64b : L.field) + nlin);
+    }
 
     // interp's frac == 0 shortcut (spectral.cpp:179-205) needs no select here:
     // a + 0 * (b - a) == a for finite table values (k is validated finite; a
@@ -949,6 +989,7 @@ struct Fp64Lean {
       rp->w = left;
       lin = nlin;
       t_cur = t_next;
+      w_cur = w_next;
       return kContinue;
     }
     if (periodic) {
@@ -959,6 +1000,7 @@ struct Fp64Lean {
         if (kPos && a == axis) pos[a] += rec.z > 0 ? -ext : ext;
       lin = nlin;
       t_cur = t_next;
+      w_cur = w_next;
       return kContinue;
     }
     // Wall exchange, absorption or reflection (tracer.cpp:155-184); the ray
@@ -1072,21 +1114,54 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     pool_kernel_body<Fp64Fast, false>(P);
 }
 
-template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true>
+template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
-  pool_kernel_body<Fp64Lean<kHint, kBrick, kPos>, false>(P);
+  pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
 }
 
 // Multigrid variant of the lean tracer (n_levels > 1).
-template <int kMinBlocks, bool kReflect = true>
+template <int kMinBlocks, bool kReflect = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
-  pool_kernel_body<Fp64Lean<0, false, true, true, kReflect>, true>(P);
+  pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
+}
+
+// Cell words of one level (TraceParams::cw_*), with the reference lookup
+// (t_lookup, spectral.cpp:148-177) and a per-cell check that the tracer's
+// decode returns exactly its (lo, frac); *bad is set if any cell does not
+// fit (the solve then keeps the temperature-reading tracers).
+__global__ void build_cell_words(const __grid_constant__ TraceParams P,
+                                 const double* __restrict__ field, int64_t n, double scale,
+                                 uint64_t* __restrict__ out, int* __restrict__ bad) {
+  bool all_ok = true;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double T = field[i];
+    int lo = 0;
+    double frac = 0.0;
+    bool ok = t_lookup(P, T, lo, frac) && lo < (1 << (64 - kCwShift));
+    uint64_t w = 0;
+    if (ok) {
+      const double ms = (T - __ldg(P.temps + lo)) * scale;  // exact power-of-two scaling
+      ok = ms >= 0.0 && ms < 9007199254740992.0 && ms == floor(ms);
+      if (ok) {
+        const uint64_t m = static_cast<uint64_t>(ms);
+        w = (static_cast<uint64_t>(lo) << kCwShift) | m;
+        int dlo;
+        double dfrac;
+        decode_cw(P, w, dlo, dfrac);
+        ok = (m >> kCwShift) == 0 && dlo == lo && dfrac == frac;
+      }
+    }
+    out[i] = w;
+    all_ok = all_ok && ok;
+  }
+  if (__any_sync(kFull, !all_ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
 // Copies the fp64 k-fastest field into the 2x2x2 micro-brick layout.
@@ -1347,6 +1422,23 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   const bool brick = P.brick && P.lv[0].field64b;
   if (min_blocks <= 0) min_blocks = P.n_levels > 1 ? (P.track_pos ? 6 : 7) : !P.track_pos ? 8 : 7;
   min_blocks = min(max(min_blocks, 6), 8);
+  if (P.cellw) {
+    if (P.n_levels > 1) {
+      if (!P.track_pos)
+        return min_blocks >= 8   ? trace_pool_fp64_lean_mg<8, false, true>
+               : min_blocks == 7 ? trace_pool_fp64_lean_mg<7, false, true>
+                                 : trace_pool_fp64_lean_mg<6, false, true>;
+      return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7, true, true>
+                             : trace_pool_fp64_lean_mg<6, true, true>;
+    }
+    if (!P.track_pos)
+      return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, false, true>
+             : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, false, true>
+                               : trace_pool_fp64_lean<6, 0, false, false, true>;
+    return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, true, true>
+           : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, true, true>
+                             : trace_pool_fp64_lean<6, 0, false, true, true>;
+  }
   if (P.n_levels > 1) {
     if (!P.track_pos)  // black walls: no reflection code
       return min_blocks >= 8   ? trace_pool_fp64_lean_mg<8, false>
@@ -1463,6 +1555,16 @@ cudaError_t launch_build_iv64(const double* k, const double* ib, int nb, int nq,
   if (n <= 0) return cudaSuccess;
   build_iv64<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
       k, ib, nb, nq, nt, iv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_cell_words(const TraceParams& P, const double* field, int64_t n,
+                                    double scale, uint64_t* out, int* bad,
+                                    cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t want = (n + 255) / 256;
+  build_cell_words<<<static_cast<unsigned>(want < 8192 ? want : 8192), 256, 0, stream>>>(
+      P, field, n, scale, out, bad);
   return cudaGetLastError();
 }
 

@@ -91,14 +91,14 @@ def test_many_chunks_offset_range_matches_reference(precision, monkeypatch):
 
 
 def _grey_slab_with_bad_ib(node_t):
-    """Grey 24x8x8 slab, kappa 50 (rays die within ~5 cells), Ib of band 0
-    set to +inf at the temperature node `node_t`."""
+    """Grey 24x8x8 slab, kappa 50 (rays die within ~5 cells), Ib of every
+    band set to +inf at the temperature node `node_t`."""
     grid = capi.make_grid((24, 8, 8), (1.0 / 24, 1.0 / 8, 1.0 / 8))
     model = E.grey_model(50.0, E.make_planck_bands(900.0, 1100.0, 8),
                          E.make_temp_grid(900.0, 1100.0, 10.0))
     ma = capi.model_from_ermc(model)
     ib = ma.ib_table.reshape(ma.n_bands, -1).copy()
-    ib[0, int(round((node_t - 900.0) / 10.0))] = np.inf
+    ib[:, int(round((node_t - 900.0) / 10.0))] = np.inf
     ma = capi.ModelArrays(ma.nu_lo, ma.nu_hi, ma.nu_center, ma.g_points, ma.g_weights,
                           ma.temps, ma.k_table, ib)
     b = capi.make_boundary((capi.WALL, capi.PERIODIC, capi.PERIODIC),
@@ -108,7 +108,7 @@ def _grey_slab_with_bad_ib(node_t):
 
 
 def test_error_in_a_later_chunk_has_the_reference_message(monkeypatch):
-    # Ib(band 0, 930 K) = inf: only rays that enter the 925 K planes x >= 20
+    # Ib(930 K) = inf: only rays that enter the 925 K planes x >= 20
     # fail; those start at x >= 15, i.e. in the last chunks.
     grid, m, b = _grey_slab_with_bad_ib(930.0)
     t = np.full(24 * 64, 950.0)
@@ -129,7 +129,7 @@ def test_error_in_a_later_chunk_has_the_reference_message(monkeypatch):
 
 @pytest.mark.parametrize("precision", [capi.FP64, capi.FP32])
 def test_nonfinite_ib_beside_an_exact_node_succeeds_like_the_reference(precision):
-    # Ib(band 0, 1010 K) = inf; every cell sits exactly on the 1000 K or
+    # Ib(1010 K) = inf; every cell sits exactly on the 1000 K or
     # 950 K node, T_max = 1000 K: interp returns the node value (frac == 0)
     # and never touches the inf — the reference solves without error.
     grid, m, b = _grey_slab_with_bad_ib(1010.0)

@@ -11,7 +11,7 @@ IFS=',' read -ra VS <<< "${VARIANTS:-ERMC_SORT=1}"
 i=0
 for V in "${VS[@]}"; do for P in ${PRECS:-fp64 fp32}; do
   F=$OUT/bench_${TAG}_v${i}_$P.json
-  env $V timeout 600 python bench.py --precision $P --steps 2 --warmup 3 --no-e2e --no-fp32-extra --cpu-seconds 1 ${BENCH_ARGS:-} > $F 2>&1
+  env $V timeout 600 python bench.py --precision $P --steps 2 --warmup 3 --no-e2e --no-fp32-extra --no-cpu --no-parity ${BENCH_ARGS:-} > $F 2>&1
   echo "[$V] $P $(python -c "
 import json,sys
 d=json.loads(open('$F').read().splitlines()[-1]); print('%.4g'%d['value'], '%.4f'%d['roofline']['frac'], '%.1f'%d['roofline']['kernel_ms_per_step'], '%.1f'%d['ms_per_step'])")"

@@ -20,11 +20,11 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   for P in fp64 fp32; do
     timeout 900 $NCU --set full --clock-control none --import-source on -k regex:trace_pool -s 1 -c 1 \
       -o $OUT/prof_${P}_$TAG -f python bench.py --grid 256 --rays 16 --precision $P --steps 1 --warmup 1 \
-      --no-e2e --no-fp32-extra --cpu-seconds 1 > $OUT/ncu_full_${P}_$TAG.log 2>&1
+      --no-e2e --no-fp32-extra --no-cpu --no-parity > $OUT/ncu_full_${P}_$TAG.log 2>&1
   done
   timeout 600 $NCU --set full --clock-control none --import-source on -k regex:ng_tile_sort -s 1 -c 1 \
     -o $OUT/prof_sort_$TAG -f python bench.py --grid 256 --rays 64 --precision fp32 --steps 1 --warmup 1 \
-    --no-e2e --no-fp32-extra --cpu-seconds 1 > $OUT/ncu_sort_$TAG.log 2>&1
+    --no-e2e --no-fp32-extra --no-cpu --no-parity > $OUT/ncu_sort_$TAG.log 2>&1
 fi
 if [ "${SKIP_CONFIGS:-1}" != "1" ]; then
   rm -f $OUT/configs_$TAG.jsonl
