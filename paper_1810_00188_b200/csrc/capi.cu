@@ -1084,9 +1084,9 @@ void session_finish(ermc_session* s, int64_t* steps_out) {
   const int R = pd.rays;
   for (int64_t ch = 0; ch < n_chunks; ++ch) {
     const unsigned long long key = counters[2 * ch + 1];
-    if (key == 0ull) continue;
+    if (key == 0ull) continue;  // raise_error stores ~(failing work id)
     const int64_t c0 = pd.lo + ch * pd.chunk_cells;
-    const uint64_t w = key - 1;
+    const uint64_t w = ~key;
     const int64_t cell = c0 + static_cast<int64_t>(w / R);
     const uint32_t ray = static_cast<uint32_t>(w % R);
     // Describe with the fp64 debug tracer (reference arithmetic).

@@ -193,11 +193,14 @@ __device__ __forceinline__ void decode_cell(const LevelDesc& L, int64_t cell,
   }
 }
 
+// Records the smallest failing work id of the chunk: the word holds ~key
+// (0 = no error; the counters are zeroed before the launch), so the maximum
+// of the complements is the minimum key.
 __device__ __forceinline__ void raise_error(const TraceParams& P, uint64_t key,
                                             int code) {
-  const unsigned long long old =
-      atomicMin(P.err_key, static_cast<unsigned long long>(key + 1));
-  if (old == 0ull || old > key + 1) atomicExch(P.err_code, code);
+  const unsigned long long enc = ~static_cast<unsigned long long>(key);
+  const unsigned long long old = atomicMax(P.err_key, enc);
+  if (old < enc) atomicExch(P.err_code, code);
 }
 
 // Tracer::kWideLevelSteps (optional): the multigrid per-level step counter

@@ -113,7 +113,7 @@ struct TraceParams {
   unsigned long long* work_counter;
   double* q_ray;             // [rays][n_cells] per-ray q contributions
   unsigned long long* steps_per_level;  // [n_levels]
-  unsigned long long* err_key;          // min failing work item + 1 (0 = none)
+  unsigned long long* err_key;          // ~(min failing work item) (0 = none)
   int32_t* err_code;
 };
 
