@@ -384,6 +384,7 @@ struct ermc_session {
       d_ibmax;
   DevBuf<float> d_wall_ibn32;
   DevBuf<double4> d_tint, d_iv64;
+  DevBuf<double2> d_pref_den;
   DevBuf<double> d_field;
   std::vector<std::unique_ptr<DevBuf<double>>> d_levels;  // levels >= 1
   std::vector<ermc_grid_t> level_grids;
@@ -566,6 +567,7 @@ struct Prepared {
   double t_max = 0.0;
   double qe = 0.0;
   std::vector<double> band_cdf, quad_cdf, kmax, ibmax, wall_ib;
+  std::vector<double2> pref_den;
   std::vector<float> wall_ibn32;
   bool sorted = false;  // narrow-band sorted dispatch enabled for this solve
 };
@@ -661,6 +663,17 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   s->d_quad_cdf.upload(pr.quad_cdf.data(), pr.quad_cdf.size(), st);
   s->d_kmax.upload(pr.kmax.data(), pr.kmax.size(), st);
   s->d_ibmax.upload(pr.ibmax.data(), pr.ibmax.size(), st);
+  // R_I denominators k(n,g,T_max) Ib(n,T_max) (sampling.cpp:93) and their
+  // correctly rounded reciprocals; non-positive ones keep the IEEE path.
+  pr.pref_den.resize(pr.kmax.size());
+  for (int n = 0; n < v.nb; ++n)
+    for (int g = 0; g < v.nq; ++g) {
+      const size_t i = static_cast<size_t>(n) * v.nq + g;
+      const double d = pr.kmax[i] * pr.ibmax[n];
+      pr.pref_den[i] = make_double2(pr.kmax[i] > 0.0 && pr.ibmax[n] > 0.0 ? d : 0.0,
+                                    d > 0.0 ? 1.0 / d : 0.0);
+    }
+  s->d_pref_den.upload(pr.pref_den.data(), pr.pref_den.size(), st);
   s->d_wall_ib.upload(pr.wall_ib.data(), pr.wall_ib.size(), st);
   // fp32 kernel: wall blackbodies normalised like its interval table.
   pr.wall_ibn32.assign(pr.wall_ib.size(), 0.0f);
@@ -742,6 +755,23 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.band_cdf = s->d_band_cdf.p;
   P.quad_cdf = s->d_quad_cdf.p;
   P.k_max = s->d_kmax.p;
+  P.pref_den = s->d_pref_den.p;
+  {
+    auto fast_div = [](uint32_t d) {
+      ermc_dev::FastDiv f{};
+      f.d = d;
+      uint32_t sh = 0;
+      while ((1ull << sh) < d) ++sh;
+      f.s = sh;
+      f.m = static_cast<uint32_t>(((1ull << 32) * ((1ull << sh) - d)) / d + 1);
+      return f;
+    };
+    const ermc_grid_t& g0 = s->grid;
+    const uint64_t nyz = static_cast<uint64_t>(g0.ny) * g0.nz;
+    P.div_rays = fast_div(static_cast<uint32_t>(c.rays_per_cell));
+    P.div_nyz = fast_div(nyz < (1ull << 31) ? static_cast<uint32_t>(nyz) : 1u);
+    P.div_nz = fast_div(static_cast<uint32_t>(g0.nz));
+  }
   P.ib_max = s->d_ibmax.p;
   P.qe = qe;
   P.tol = c.tolerance;

@@ -176,16 +176,24 @@ __device__ __forceinline__ void sample_band(const TraceParams& P, double r_n,
   if (g >= P.n_quad) g = P.n_quad - 1;
 }
 
-// Linear k-fastest index -> (i, j, k) (reference solver.cpp:120-122).
-__device__ __forceinline__ void decode_cell(const LevelDesc& L, int64_t cell,
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (__umulhi(n, f.m) + n) >> f.s;
+}
+
+// Linear k-fastest index of a level-0 cell -> (i, j, k) (reference
+// solver.cpp:120-122); invariant-divisor divisions below 2^31 cells.
+__device__ __forceinline__ void decode_cell(const TraceParams& P, int64_t cell,
                                             int& ci, int& cj, int& ck) {
+  const LevelDesc& L = P.lv[0];
   const int64_t nyz = static_cast<int64_t>(L.n[1]) * L.n[2];
   if (cell < 0x7fffffffLL && nyz < 0x7fffffffLL) {
     const uint32_t c = static_cast<uint32_t>(cell);
-    const uint32_t nz = static_cast<uint32_t>(L.n[2]);
-    ci = static_cast<int>(c / static_cast<uint32_t>(nyz));
-    cj = static_cast<int>((c / nz) % static_cast<uint32_t>(L.n[1]));
-    ck = static_cast<int>(c % nz);
+    const uint32_t i = fdiv(c, P.div_nyz);
+    const uint32_t rem = c - i * static_cast<uint32_t>(nyz);
+    const uint32_t j = fdiv(rem, P.div_nz);
+    ci = static_cast<int>(i);
+    cj = static_cast<int>(j);
+    ck = static_cast<int>(rem - j * static_cast<uint32_t>(L.n[2]));
   } else {
     ci = static_cast<int>(cell / nyz);
     cj = static_cast<int>((cell / L.n[2]) % L.n[1]);
@@ -273,7 +281,7 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
           w = nb + (rank - avail);
         if (w != 0xffffffffu) {
           if (P.perm) w = __ldg(P.perm + w);  // narrow-band sorted order
-          const uint32_t cell = w / rays;
+          const uint32_t cell = fdiv(w, P.div_rays);
           my_work = w;
           const int e = tr.init(P, P.cell_base + cell, w - cell * rays);
           if (e == kErrNone)
@@ -317,7 +325,7 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         if (st == kDone) {
           const double q = tr.finish(P);
           if (isfinite(q) && tr.finite_state()) {
-            const uint32_t cell = my_work / rays;
+            const uint32_t cell = fdiv(my_work, P.div_rays);
             const uint32_t ray = my_work - cell * rays;
             // streaming store: keep the L2 for the temperature field
             __stcs(P.q_ray + static_cast<uint64_t>(ray) * P.n_cells + cell, q);

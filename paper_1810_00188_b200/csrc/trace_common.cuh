@@ -15,6 +15,14 @@ constexpr int kMaxLevels = 16;
 constexpr int kMaxSmemCdf = 2048;  // sampling CDFs staged in shared memory up to
                                    // this many doubles (16 KB; 119 x 16 needs 2023)
 
+// Division by a loop-invariant divisor d >= 1 for numerators n < 2^31:
+// q = (umulhi(n, m) + n) >> s with s = ceil(log2 d),
+// m = floor(2^32 (2^s - d) / d) + 1 (Granlund-Montgomery); 3 instructions
+// instead of the ~18 of a runtime 32-bit division.
+struct FastDiv {
+  uint32_t d, m, s, pad;
+};
+
 // One multigrid level (reference GridHierarchy, geometry.hpp:74-83).
 struct LevelDesc {
   int32_t n[3];      // cells per axis
@@ -98,6 +106,10 @@ struct TraceParams {
   int32_t volume_sampling;
   uint64_t h_seed;           // mix64(seed + 0x9e3779b97f4a7c15) (sampling.cpp:25)
   int32_t rays;              // rays per cell
+
+  // ---- per-ray setup helpers (bitwise the reference's arithmetic) ----
+  FastDiv div_rays, div_nyz, div_nz;  // work id -> (cell, ray); level-0 cell decode
+  const double2* pref_den;   // [n_bands*n_quad] {k(n,g,T_max) Ib(n,T_max), RN(1 / that)}
 
   // ---- work decomposition ----
   int32_t refill_threshold;  // idle lanes before a warp regenerates rays

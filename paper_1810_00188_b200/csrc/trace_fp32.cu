@@ -122,7 +122,7 @@ struct Fp32Tracer {
                                       uint32_t ray, const double* cdf = nullptr) {
     const LevelDesc& L = P.lv[0];
     int ci, cj, ck;
-    decode_cell(L, cell, ci, cj, ck);
+    decode_cell(P, cell, ci, cj, ck);
     h_cell = mix64(P.h_seed ^ static_cast<uint64_t>(cell));
     ray_id = ray;
     const double r_theta = draw_u(h_cell, ray, 0);

@@ -93,7 +93,7 @@ def base(name, grid, cfg, steps, ms, tms, prec):
     return dict(config=name, grid=[grid.nx, grid.ny, grid.nz], rays=cfg.rays_per_cell,
                 precision=prec, n_levels=cfg.n_levels, total_steps=tot,
                 steps_per_ray=tot / (n * cfg.rays_per_cell), solve_ms=ms,
-                trace_ms=tms[2], sort_ms=tms[1], reduce_ms=tms[3],
+                trace_ms=tms[2], sort_ms=tms[1], reduce_ms=tms[3], setup_ms=tms[0],
                 steps_per_s=tot / (ms * 1e-3), trace_steps_per_s=tot / (tms[2] * 1e-3))
 
 
