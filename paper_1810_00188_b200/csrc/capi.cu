@@ -385,6 +385,7 @@ struct ermc_session {
   DevBuf<float> d_wall_ibn32;
   DevBuf<double4> d_tint, d_iv64;
   DevBuf<double2> d_pref_den;
+  DevBuf<uint8_t> d_cdf_guide;
   DevBuf<double> d_field;
   std::vector<std::unique_ptr<DevBuf<double>>> d_levels;  // levels >= 1
   std::vector<ermc_grid_t> level_grids;
@@ -659,6 +660,25 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
           pr.wall_ib[(2 * a + side) * static_cast<size_t>(v.nb) + n] =
               ermc_host::interp_ib(v, n, wt[side]);
   }
+  {  // guide tables of the staged CDFs (device_common.cuh sample_band_cdf)
+    std::vector<uint8_t> guide(ermc_dev::kGuideBand + static_cast<size_t>(v.nb) *
+                                                          ermc_dev::kGuideQuad);
+    for (int k = 0; k < ermc_dev::kGuideBand; ++k)
+      guide[k] = static_cast<uint8_t>(std::min<ptrdiff_t>(
+          255, std::upper_bound(pr.band_cdf.begin(), pr.band_cdf.end(),
+                                static_cast<double>(k) / ermc_dev::kGuideBand) -
+                   pr.band_cdf.begin()));
+    for (int n = 0; n < v.nb; ++n) {
+      auto q0 = pr.quad_cdf.begin() + static_cast<ptrdiff_t>(n) * v.nq;
+      for (int k = 0; k < ermc_dev::kGuideQuad; ++k)
+        guide[ermc_dev::kGuideBand + n * ermc_dev::kGuideQuad + k] = static_cast<uint8_t>(
+            std::min<ptrdiff_t>(255, std::upper_bound(q0, q0 + v.nq,
+                                                      static_cast<double>(k) /
+                                                          ermc_dev::kGuideQuad) -
+                                         q0));
+    }
+    s->d_cdf_guide.upload(guide.data(), guide.size(), st);
+  }
   s->d_band_cdf.upload(pr.band_cdf.data(), pr.band_cdf.size(), st);
   s->d_quad_cdf.upload(pr.quad_cdf.data(), pr.quad_cdf.size(), st);
   s->d_kmax.upload(pr.kmax.data(), pr.kmax.size(), st);
@@ -800,7 +820,9 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.t_first = v.temps[0];
   P.t_last = v.temps[v.nt - 1];
   P.steps_per_level = s->d_steps.p;
-  P.cdf_smem = tune().cdf_smem && v.nb * (1 + v.nq) <= ermc_dev::kMaxSmemCdf ? 1 : 0;
+  P.cdf_smem = tune().cdf_smem && v.nb * (1 + v.nq) <= ermc_dev::kMaxSmemCdf &&
+                       v.nb <= 255 && v.nq <= 255 ? 1 : 0;
+  P.cdf_guide = s->d_cdf_guide.p;
   // Positions matter after a wall only if some wall can reflect.
   P.track_pos = 0;
   for (int a = 0; a < 3; ++a)

@@ -150,19 +150,37 @@ __device__ __forceinline__ int upper_bound_gen(const double* a, int n, double x)
 // latency instead of dependent global loads. Layout: band_cdf[nb] then
 // quad_cdf[nb][nq], right after the kernel's per-thread records.
 
+// Bytes of the staged CDFs and their guide tables (16-byte multiple).
+__host__ __device__ inline size_t cdf_smem_bytes(int nb, int nq) {
+  const size_t guide = (static_cast<size_t>(kGuideBand) + static_cast<size_t>(nb) * kGuideQuad +
+                        15) / 16 * 16;
+  return static_cast<size_t>(nb) * (1 + nq) * sizeof(double) + guide;
+}
+
 __device__ __forceinline__ void stage_cdfs(const TraceParams& P, double* dst) {
   const int nb = P.n_bands, n = nb + nb * P.n_quad;
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     dst[i] = i < nb ? P.band_cdf[i] : P.quad_cdf[i - nb];
+  uint8_t* gdst = reinterpret_cast<uint8_t*>(dst + n);
+  for (int i = threadIdx.x; i < kGuideBand + nb * kGuideQuad; i += blockDim.x)
+    gdst[i] = P.cdf_guide[i];
   __syncthreads();
 }
 
+// sample_band (sampling.cpp:42-53) on the staged CDFs: upper_bound by a
+// linear scan from the guide bucket's start (the same index: upper_bound is
+// monotone in r and r >= bucket start; ~1-2 compares instead of log2 n).
+// r * 64 and r * 16 are exact, so the bucket of r is floor(r * G).
 __device__ __forceinline__ void sample_band_cdf(const TraceParams& P, const double* cdf,
                                                 double r_n, double r_g, int& n, int& g) {
   const int nb = P.n_bands, nq = P.n_quad;
-  n = upper_bound_gen(cdf, nb, r_n);
+  const uint8_t* guide = reinterpret_cast<const uint8_t*>(cdf + nb + nb * nq);
+  n = guide[static_cast<int>(r_n * kGuideBand)];
+  while (n < nb && !(r_n < cdf[n])) ++n;
   if (n >= nb) n = nb - 1;
-  g = upper_bound_gen(cdf + nb + n * nq, nq, r_g);
+  const double* qc = cdf + nb + n * nq;
+  g = guide[kGuideBand + n * kGuideQuad + static_cast<int>(r_g * kGuideQuad)];
+  while (g < nq && !(r_g < qc[g])) ++g;
   if (g >= nq) g = nq - 1;
 }
 

@@ -14,6 +14,12 @@ namespace ermc_dev {
 constexpr int kMaxLevels = 16;
 constexpr int kMaxSmemCdf = 2048;  // sampling CDFs staged in shared memory up to
                                    // this many doubles (16 KB; 119 x 16 needs 2023)
+// Guide tables of the staged CDFs (sample_band_cdf): the band CDF is split
+// in kGuideBand equal buckets of [0, 1), each g CDF in kGuideQuad; a bucket
+// holds upper_bound(cdf, bucket start), where the search for any r in the
+// bucket can start.
+constexpr int kGuideBand = 64;
+constexpr int kGuideQuad = 16;
 
 // Division by a loop-invariant divisor d >= 1 for numerators n < 2^31:
 // q = (umulhi(n, m) + n) >> s with s = ceil(log2 d),
@@ -79,6 +85,7 @@ struct TraceParams {
   double inv_dt;             // 1/dt for the table-index estimate
   double inv_w;              // RN(1 / dt): tint's reciprocal when tint_arith
   int32_t cdf_smem;          // lean kernels stage the sampling CDFs in shared memory
+  const uint8_t* cdf_guide;  // [kGuideBand + n_bands * kGuideQuad] (with cdf_smem)
   int32_t tint_arith;        // every node is exactly l*dt + t0 and every width
                              // exactly dt, so tint[l] is computed, not loaded
   double t_first, t_last;    // table range

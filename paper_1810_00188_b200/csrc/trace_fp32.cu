@@ -892,7 +892,7 @@ bool fp32_lean(const TraceParams& P) { return P.lean != 0; }
 size_t fp32_smem(const TraceParams& P) {
   if (!fp32_lean(P)) return 0;
   return kRecs32 * kBlock32 * sizeof(int4) +
-         (P.cdf_smem ? static_cast<size_t>(P.n_bands) * (1 + P.n_quad) * sizeof(double) : 0);
+         (P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad) : 0);
 }
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   // 8 blocks/SM (64 registers) measured best; 10 and 12 lose (0.98, 0.92x).

@@ -1425,7 +1425,7 @@ bool lean_path(const TraceParams& P) {
 size_t fp64_smem(const TraceParams& P) {
   if (!lean_path(P)) return 0;
   return kLeanRecs64 * kBlock * sizeof(int4) +
-         (P.cdf_smem ? static_cast<size_t>(P.n_bands) * (1 + P.n_quad) * sizeof(double) : 0);
+         (P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad) : 0);
 }
 // min_blocks = 0 picks the measured best per variant (B200, 256^3 channel):
 // 8 blocks/SM for the black-wall tracer (64 registers + 128 B of L1-resident
