@@ -922,9 +922,9 @@ void ensure_cell_words(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
   P.cw_shift = 56;
   P.cw_dt = cw_dt;
   P.cw_rdt = 1.0 / cw_dt;
-  // Pair layout along the axis with the smallest spacing (most crossings
+  // Sector layout along the axis with the smallest spacing (most crossings
   // for isotropic rays; ties to the faster-varying axis) when every level
-  // has an even number of cells on it.
+  // has a multiple of 4 cells on it.
   {
     const ermc_grid_t& g0 = s->grid;
     const double d[3] = {g0.dx, g0.dy, g0.dz};
@@ -934,7 +934,7 @@ void ensure_cell_words(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
     bool fits = tune().cellw_sec != 0;
     for (const ermc_grid_t& g : s->level_grids) {
       const int n[3] = {g.nx, g.ny, g.nz};
-      fits = fits && n[G] % 2 == 0;  // trace_fp64.cu kSecW
+      fits = fits && n[G] % 4 == 0;
     }
     P.cw_sec = fits ? 1 : 0;
     P.sec_axis = G;

@@ -96,11 +96,11 @@ struct TraceParams {
   int32_t cellw;             // 1: the lean fp64 tracers read cell words
   int32_t cw_shift;          // lo = w >> cw_shift (64 - bits of the interval index)
   double cw_dt, cw_rdt;
-  // cw_sec: every level's words are stored in aligned groups of kSecW = 2
-  // cells consecutive along axis sec_axis (the most-stepped one): group
-  // index in k-fastest order over the grid with n[sec_axis] / 2 groups on
-  // that axis, word index = 2 * group + (index on sec_axis & 1). A tracer
-  // keeps its cell's group in registers and loads a new one only on leaving it.
+  // cw_sec: every level's words are stored in 32-byte sectors of 4 cells
+  // consecutive along axis sec_axis (the most-stepped one): sector index in
+  // k-fastest order over the grid with n[sec_axis] / 4 sectors on that axis,
+  // word index = 4 * sector + (index on sec_axis & 3). A tracer keeps its
+  // cell's sector in registers and loads a new one only on leaving it.
   int32_t cw_sec;
   int32_t sec_axis;
 

@@ -427,29 +427,27 @@ __device__ __forceinline__ void decode_cw(const TraceParams& P, uint64_t w, int&
   frac = div_rcp(static_cast<double>(m), P.cw_dt, P.cw_rdt);
 }
 
-// Sector layout of the cell words (TraceParams::cw_sec): kSecW consecutive
-// cells along sec_axis per aligned group, loaded with one vector load.
-// Measured (r2i): 4-cell groups (32 B, LDG.256) lose — a 32-byte-per-lane
-// load of scattered lanes costs the L1 twice the wavefronts of an 8-byte one
-// — so groups are pairs (16 B: LDG.128, one wavefront per lane like 8 B).
-constexpr int kSecW = 2, kSecShift = 1;
+// Sector layout of the cell words (TraceParams::cw_sec).
 __device__ __forceinline__ int sec_count(const LevelDesc& L, int G, int a) {
-  return a == G ? (L.n[a] >> kSecShift) : L.n[a];
+  return a == G ? (L.n[a] >> 2) : L.n[a];
 }
 __device__ __forceinline__ int sec_index(const LevelDesc& L, int G, int i, int j, int k) {
-  const int si = G == 0 ? i >> kSecShift : i, sj = G == 1 ? j >> kSecShift : j,
-            sk = G == 2 ? k >> kSecShift : k;
+  const int si = G == 0 ? i >> 2 : i, sj = G == 1 ? j >> 2 : j, sk = G == 2 ? k >> 2 : k;
   return (si * sec_count(L, G, 1) + sj) * sec_count(L, G, 2) + sk;
 }
 __device__ __forceinline__ int sec_word(const LevelDesc& L, int G, int i, int j, int k) {
-  const int sub = (G == 0 ? i : G == 1 ? j : k) & (kSecW - 1);
-  return sec_index(L, G, i, j, k) * kSecW + sub;
+  const int sub = (G == 0 ? i : G == 1 ? j : k) & 3;
+  return sec_index(L, G, i, j, k) * 4 + sub;
 }
-__device__ __forceinline__ void ld_sector(const uint64_t* p, uint64_t (&w)[kSecW]) {
-  asm("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(w[0]), "=l"(w[1]) : "l"(p));
+__device__ __forceinline__ void ld_sector(const uint64_t* p, uint64_t (&w)[4]) {
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+      : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+      : "l"(p));
 }
-__device__ __forceinline__ uint64_t pick_word(const uint64_t (&w)[kSecW], int sub) {
-  return sub ? w[1] : w[0];
+__device__ __forceinline__ uint64_t pick_word(const uint64_t (&w)[4], int sub) {
+  const uint64_t a = (sub & 1) ? w[1] : w[0];
+  const uint64_t b = (sub & 1) ? w[3] : w[2];
+  return (sub & 2) ? b : a;
 }
 
 // init_ray (reference sampling.cpp:55-96) for global cell `cell`, with the
@@ -833,7 +831,7 @@ struct Fp64Lean {
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
   uint64_t w_cur;  // kCW: the current cell's word
-  uint64_t sw[kSecW];  // kSec: the current cell's group of words
+  uint64_t sw[4];  // kSec: the current cell's sector
   int sub;         // kSec: the cell's place in it
   int4* ax;
   int row;  // first interval record of (band, g) in iv64
@@ -876,7 +874,7 @@ struct Fp64Lean {
     }
     if (kSec) {
       lin = sec_index(L, G, idx[0], idx[1], idx[2]);
-      sub = (G == 0 ? idx[0] : G == 1 ? idx[1] : idx[2]) & (kSecW - 1);
+      sub = (G == 0 ? idx[0] : G == 1 ? idx[1] : idx[2]) & 3;
     } else {
       lin = kBrick ? brick_index(L, idx[0], idx[1], idx[2])
                    : (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
@@ -911,7 +909,7 @@ struct Fp64Lean {
                                static_cast<int>(cell), static_cast<int>(ray));
     if (kSec) {
       setup(P.lv[0], r.idx, P.sec_axis);
-      ld_sector(P.lv[0].cellw + kSecW * lin, sw);
+      ld_sector(P.lv[0].cellw + 4 * lin, sw);
       return kErrNone;
     }
     if (kCW)
@@ -947,7 +945,7 @@ struct Fp64Lean {
     sal_ = 0;
     if (kSec) {
       setup(C, idx, P.sec_axis);
-      ld_sector(C.cellw + kSecW * lin, sw);
+      ld_sector(C.cellw + 4 * lin, sw);
       return kErrNone;
     }
     setup(C, idx);
@@ -1017,8 +1015,8 @@ struct Fp64Lean {
       nlin = lin + rec.z;
       if (axis == G) {  // along the sector axis: a new sector only past its end
         const int ns = sub + (rec.z > 0 ? 1 : -1);
-        nsub = ns & (kSecW - 1);
-        if (static_cast<unsigned>(ns) < static_cast<unsigned>(kSecW)) nlin = lin;
+        nsub = ns & 3;
+        if (static_cast<unsigned>(ns) < 4u) nlin = lin;
       }
       if (!inside) nlin -= rec.z * sec_count(L, G, axis);  // periodic image
     } else {
@@ -1029,7 +1027,7 @@ struct Fp64Lean {
     uint64_t w_next = w_cur;
     if (inside || periodic) {
       if (kSec) {
-        if (nlin != lin) ld_sector(L.cellw + kSecW * nlin, sw);
+        if (nlin != lin) ld_sector(L.cellw + 4 * nlin, sw);
       } else if (kCW) {
         w_next = __ldg(L.cellw + nlin);
       } else {
@@ -1239,7 +1237,7 @@ __global__ void build_cell_words(const __grid_constant__ TraceParams P, const Le
         ok = (m >> kCwShift) == 0 && dlo == lo && dfrac == frac;
       }
     }
-    if (P.cw_sec) {  // group layout of this level (n[sec_axis] % kSecW == 0, host-checked)
+    if (P.cw_sec) {  // sector layout of this level (n[sec_axis] % 4 == 0, checked on the host)
       const int64_t nyz = static_cast<int64_t>(L.n[1]) * L.n[2];
       const int ci = static_cast<int>(i / nyz);
       const int cj = static_cast<int>((i / L.n[2]) % L.n[1]);
