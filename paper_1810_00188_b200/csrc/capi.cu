@@ -63,9 +63,8 @@ cudaError_t launch_to_fp32_bricked(const double* src, float* dst, int nx, int ny
                                    int nz, int b, cudaStream_t s);
 cudaError_t launch_to_bricked64(const double* src, double* dst, int nx, int ny, int nz,
                                 cudaStream_t s);
-cudaError_t launch_build_cell_words(const TraceParams& P, int level, const double* field,
-                                    int64_t n, double scale, uint64_t* out, int* bad,
-                                    cudaStream_t s);
+cudaError_t launch_build_cell_words(const TraceParams& P, const double* field, int64_t n,
+                                    double scale, uint64_t* out, int* bad, cudaStream_t s);
 int sort_max_bins();
 int sort_max_tile_items();
 cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_rows,
@@ -336,7 +335,6 @@ struct Tune {
   int sort_block = 0;  // cubic sort tiles (edge in cells; 0 = linear tiles)
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
   int cellw = 1;       // fp64 lean tracers read precomputed cell words (trace_fp64.cu)
-  int cellw_sec = 1;   // ... in 4-cell sectors along the most-stepped axis
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -363,7 +361,6 @@ const Tune& tune() {
     x.sort_dirs = std::max(1, env_int("ERMC_SORT_DIRS", x.sort_dirs));
     x.sort_block = std::max(0, env_int("ERMC_SORT_BLOCK", x.sort_block));
     x.cellw = env_int("ERMC_CELLW", x.cellw);
-    x.cellw_sec = env_int("ERMC_CELLW_SEC", x.cellw_sec);
     return x;
   }();
   return t;
@@ -400,7 +397,6 @@ struct ermc_session {
   std::vector<std::unique_ptr<DevBuf<uint64_t>>> d_cellw;
   DevBuf<int> d_cw_bad;
   bool cellw_valid = false, cellw_ok = false;
-  int cellw_layout = -1;  // cw_sec + 2 * sec_axis of the built words
   std::vector<std::unique_ptr<DevBuf<float>>> d_levels32;
   DevBuf<float4> d_iv32;
   bool iv32_ready = false;
@@ -922,25 +918,6 @@ void ensure_cell_words(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
   P.cw_shift = 56;
   P.cw_dt = cw_dt;
   P.cw_rdt = 1.0 / cw_dt;
-  // Sector layout along the axis with the smallest spacing (most crossings
-  // for isotropic rays; ties to the faster-varying axis) when every level
-  // has a multiple of 4 cells on it.
-  {
-    const ermc_grid_t& g0 = s->grid;
-    const double d[3] = {g0.dx, g0.dy, g0.dz};
-    int G = 2;
-    for (int a = 1; a >= 0; --a)
-      if (d[a] < d[G]) G = a;
-    bool fits = tune().cellw_sec != 0;
-    for (const ermc_grid_t& g : s->level_grids) {
-      const int n[3] = {g.nx, g.ny, g.nz};
-      fits = fits && n[G] % 4 == 0;
-    }
-    P.cw_sec = fits ? 1 : 0;
-    P.sec_axis = G;
-    if (s->cellw_valid && s->cellw_layout != P.cw_sec + 2 * G) s->cellw_valid = false;
-    s->cellw_layout = P.cw_sec + 2 * G;
-  }
   if (!s->cellw_valid) {
     Timing t;
     cudaEventCreate(&t.a);
@@ -955,8 +932,8 @@ void ensure_cell_words(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
       const int64_t n = cells_of(s->level_grids[l]);
       s->d_cellw[l]->ensure(static_cast<size_t>(n));
       const double* field = l == 0 ? s->d_field.p : s->d_levels[l]->p;
-      cuda_check(ermc_dev::launch_build_cell_words(P, static_cast<int>(l), field, n, scale,
-                                                   s->d_cellw[l]->p, s->d_cw_bad.p, st),
+      cuda_check(ermc_dev::launch_build_cell_words(P, field, n, scale, s->d_cellw[l]->p,
+                                                   s->d_cw_bad.p, st),
                  "build_cell_words");
       ++s->launches;
     }

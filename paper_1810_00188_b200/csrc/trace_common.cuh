@@ -96,13 +96,6 @@ struct TraceParams {
   int32_t cellw;             // 1: the lean fp64 tracers read cell words
   int32_t cw_shift;          // lo = w >> cw_shift (64 - bits of the interval index)
   double cw_dt, cw_rdt;
-  // cw_sec: every level's words are stored in 32-byte sectors of 4 cells
-  // consecutive along axis sec_axis (the most-stepped one): sector index in
-  // k-fastest order over the grid with n[sec_axis] / 4 sectors on that axis,
-  // word index = 4 * sector + (index on sec_axis & 3). A tracer keeps its
-  // cell's sector in registers and loads a new one only on leaving it.
-  int32_t cw_sec;
-  int32_t sec_axis;
 
   // ---- fp32 fast-path tables (trace_fp32.cu) ----
   const float4* iv32;        // [n_bands*n_quad][n_temps-1] {k_lo, k_hi-k_lo, ib_lo, ib_hi-ib_lo}

@@ -427,29 +427,6 @@ __device__ __forceinline__ void decode_cw(const TraceParams& P, uint64_t w, int&
   frac = div_rcp(static_cast<double>(m), P.cw_dt, P.cw_rdt);
 }
 
-// Sector layout of the cell words (TraceParams::cw_sec).
-__device__ __forceinline__ int sec_count(const LevelDesc& L, int G, int a) {
-  return a == G ? (L.n[a] >> 2) : L.n[a];
-}
-__device__ __forceinline__ int sec_index(const LevelDesc& L, int G, int i, int j, int k) {
-  const int si = G == 0 ? i >> 2 : i, sj = G == 1 ? j >> 2 : j, sk = G == 2 ? k >> 2 : k;
-  return (si * sec_count(L, G, 1) + sj) * sec_count(L, G, 2) + sk;
-}
-__device__ __forceinline__ int sec_word(const LevelDesc& L, int G, int i, int j, int k) {
-  const int sub = (G == 0 ? i : G == 1 ? j : k) & 3;
-  return sec_index(L, G, i, j, k) * 4 + sub;
-}
-__device__ __forceinline__ void ld_sector(const uint64_t* p, uint64_t (&w)[4]) {
-  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
-      : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
-      : "l"(p));
-}
-__device__ __forceinline__ uint64_t pick_word(const uint64_t (&w)[4], int sub) {
-  const uint64_t a = (sub & 1) ? w[1] : w[0];
-  const uint64_t b = (sub & 1) ? w[3] : w[2];
-  return (sub & 2) ? b : a;
-}
-
 // init_ray (reference sampling.cpp:55-96) for global cell `cell`, with the
 // level-0 grid. Returns an error code (0 = ok).
 // cdf: the staged sampling CDFs (lean kernels) or null for P's global copy.
@@ -517,8 +494,7 @@ __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}: copies of the table values
     const double4* row = P.iv64 + (n * P.n_quad + g) * (P.n_temps - 1);
     if (kCW) {
-      const int wi = P.cw_sec ? sec_word(L, P.sec_axis, ci, cj, ck) : static_cast<int>(cell);
-      decode_cw(P, __ldg(L.cellw + wi), lo, frac);
+      decode_cw(P, __ldg(L.cellw + cell), lo, frac);
       v = ld_rec64<0>(row + lo);
     } else if (!lookup_spec<0>(P, row, __ldg(L.field + cell), lo, frac, v)) {
       return kErrTableRange;
@@ -818,21 +794,14 @@ constexpr int kLeanRecs64 = 4;
 // interval and exact offset, precomputed per field) instead of temperatures,
 // so a step decodes (lo, frac) with one shift, one mask, one conversion and
 // one Markstein quotient instead of running the table lookup.
-// kSec (with kCW): the words are in the sector layout (TraceParams::cw_sec);
-// the tracer holds its cell's 4-word sector in registers (`sw`) and `sub`,
-// and `lin` counts sectors. A step along sec_axis that stays inside the
-// sector needs no load.
 template <int kHint, bool kBrick, bool kPos = true, bool kMulti = false, bool kReflect = kPos,
-          bool kCW = false, bool kSec = false>
+          bool kCW = false>
 struct Fp64Lean {
   static_assert(!kMulti || (kPos && !kBrick), "demotion reads positions, k-fastest levels");
   static_assert(!kCW || !kBrick, "cell words use the k-fastest layout");
-  static_assert(!kSec || kCW, "sectors hold cell words");
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
   uint64_t w_cur;  // kCW: the current cell's word
-  uint64_t sw[4];  // kSec: the current cell's sector
-  int sub;         // kSec: the cell's place in it
   int4* ax;
   int row;  // first interval record of (band, g) in iv64
   int lin, steps_;
@@ -846,11 +815,10 @@ struct Fp64Lean {
   }
 
   // Dda::setup (tracer.cpp:17-38) + the per-axis records.
-  __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx, int G = 0) {
+  __device__ __forceinline__ void setup(const LevelDesc& L, const int* idx) {
     const int nby = (L.n[1] + 1) >> 1, nbz = (L.n[2] + 1) >> 1;
-    const int s1 = kSec ? sec_count(L, G, 1) : L.n[1], s2 = kSec ? sec_count(L, G, 2) : L.n[2];
-    const int stride[3] = {kBrick ? 8 * nby * nbz - 4 : s1 * s2, kBrick ? 8 * nbz - 2 : s2,
-                           kBrick ? 7 : 1};
+    const int stride[3] = {kBrick ? 8 * nby * nbz - 4 : L.n[1] * L.n[2],
+                           kBrick ? 8 * nbz - 2 : L.n[2], kBrick ? 7 : 1};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double da = dir[a];
@@ -872,13 +840,8 @@ struct Fp64Lean {
                                  pos_dir ? stride[a] : -stride[a],
                                  pos_dir ? L.n[a] - 1 - idx[a] : idx[a]);
     }
-    if (kSec) {
-      lin = sec_index(L, G, idx[0], idx[1], idx[2]);
-      sub = (G == 0 ? idx[0] : G == 1 ? idx[1] : idx[2]) & 3;
-    } else {
-      lin = kBrick ? brick_index(L, idx[0], idx[1], idx[2])
-                   : (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
-    }
+    lin = kBrick ? brick_index(L, idx[0], idx[1], idx[2])
+                 : (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
   }
 
   __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
@@ -907,11 +870,6 @@ struct Fp64Lean {
     sal_ = 0;
     ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
                                static_cast<int>(cell), static_cast<int>(ray));
-    if (kSec) {
-      setup(P.lv[0], r.idx, P.sec_axis);
-      ld_sector(P.lv[0].cellw + 4 * lin, sw);
-      return kErrNone;
-    }
     if (kCW)
       w_cur = __ldg(P.lv[0].cellw + cell);
     else
@@ -943,11 +901,6 @@ struct Fp64Lean {
       idx[a] = i;
     }
     sal_ = 0;
-    if (kSec) {
-      setup(C, idx, P.sec_axis);
-      ld_sector(C.cellw + 4 * lin, sw);
-      return kErrNone;
-    }
     setup(C, idx);
     if (kCW)
       w_cur = __ldg(C.cellw + lin);
@@ -974,7 +927,7 @@ struct Fp64Lean {
     double frac;
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
     if (kCW) {
-      decode_cw(P, kSec ? pick_word(sw, sub) : w_cur, lo, frac);
+      decode_cw(P, w_cur, lo, frac);
       v = ld_rec64<kHint>(P.iv64 + row + lo);
     } else if (!lookup_spec<kHint>(P, P.iv64 + row, t_cur, lo, frac, v)) {
       err = kErrTableRange;
@@ -994,7 +947,6 @@ struct Fp64Lean {
 
     int4* rp = ax + axis * kBlock;
     const int4 rec = *rp;
-    int nsub = kSec ? sub : 0;
     const double td = __hiloint2double(rec.y, rec.x);
     const int left = rec.w - 1;
     const bool inside = left >= 0;
@@ -1010,15 +962,6 @@ struct Fp64Lean {
           idx[a] = a == axis ? (rec.z > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
         nlin = brick_index(L, idx[0], idx[1], idx[2]);
       }
-    } else if (kSec) {
-      const int G = P.sec_axis;
-      nlin = lin + rec.z;
-      if (axis == G) {  // along the sector axis: a new sector only past its end
-        const int ns = sub + (rec.z > 0 ? 1 : -1);
-        nsub = ns & 3;
-        if (static_cast<unsigned>(ns) < 4u) nlin = lin;
-      }
-      if (!inside) nlin -= rec.z * sec_count(L, G, axis);  // periodic image
     } else {
       nlin = lin + rec.z;
       if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
@@ -1026,13 +969,10 @@ struct Fp64Lean {
     double t_next = t_cur;
     uint64_t w_next = w_cur;
     if (inside || periodic) {
-      if (kSec) {
-        if (nlin != lin) ld_sector(L.cellw + 4 * nlin, sw);
-      } else if (kCW) {
+      if (kCW)
         w_next = __ldg(L.cellw + nlin);
-      } else {
+      else
         t_next = ld_t64<kHint>((kBrick ? L.field64b : L.field) + nlin);
-      }
     }
 
     // interp's frac == 0 shortcut (spectral.cpp:179-205) needs no select here:
@@ -1066,7 +1006,6 @@ struct Fp64Lean {
       lin = nlin;
       t_cur = t_next;
       w_cur = w_next;
-      if (kSec) sub = nsub;
       return kContinue;
     }
     if (periodic) {
@@ -1078,7 +1017,6 @@ struct Fp64Lean {
       lin = nlin;
       t_cur = t_next;
       w_cur = w_next;
-      if (kSec) sub = nsub;
       return kContinue;
     }
     // Wall exchange, absorption or reflection (tracer.cpp:155-184); the ray
@@ -1137,7 +1075,7 @@ struct Fp64Lean {
       pos[0] += L.eps * dir[0];
       pos[1] += L.eps * dir[1];
       pos[2] += L.eps * dir[2];
-      setup(L, idx, kSec ? P.sec_axis : 0);
+      setup(L, idx);
       return kContinue;
     }
   }
@@ -1192,29 +1130,28 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     pool_kernel_body<Fp64Fast, false>(P);
 }
 
-template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = false,
-          bool kSec = false>
+template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
-  pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW, kSec>, false>(P);
+  pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
 }
 
 // Multigrid variant of the lean tracer (n_levels > 1).
-template <int kMinBlocks, bool kReflect = true, bool kCW = false, bool kSec = false>
+template <int kMinBlocks, bool kReflect = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
-  pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW, kSec>, true>(P);
+  pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
 }
 
 // Cell words of one level (TraceParams::cw_*), with the reference lookup
 // (t_lookup, spectral.cpp:148-177) and a per-cell check that the tracer's
 // decode returns exactly its (lo, frac); *bad is set if any cell does not
 // fit (the solve then keeps the temperature-reading tracers).
-__global__ void build_cell_words(const __grid_constant__ TraceParams P, const LevelDesc L,
+__global__ void build_cell_words(const __grid_constant__ TraceParams P,
                                  const double* __restrict__ field, int64_t n, double scale,
                                  uint64_t* __restrict__ out, int* __restrict__ bad) {
   bool all_ok = true;
@@ -1237,15 +1174,7 @@ __global__ void build_cell_words(const __grid_constant__ TraceParams P, const Le
         ok = (m >> kCwShift) == 0 && dlo == lo && dfrac == frac;
       }
     }
-    if (P.cw_sec) {  // sector layout of this level (n[sec_axis] % 4 == 0, checked on the host)
-      const int64_t nyz = static_cast<int64_t>(L.n[1]) * L.n[2];
-      const int ci = static_cast<int>(i / nyz);
-      const int cj = static_cast<int>((i / L.n[2]) % L.n[1]);
-      const int ck = static_cast<int>(i % L.n[2]);
-      out[sec_word(L, P.sec_axis, ci, cj, ck)] = w;
-    } else {
-      out[i] = w;
-    }
+    out[i] = w;
     all_ok = all_ok && ok;
   }
   if (__any_sync(kFull, !all_ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
@@ -1511,21 +1440,6 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   if (min_blocks <= 0)
     min_blocks = P.n_levels > 1 ? (P.track_pos ? 6 : 7) : !P.track_pos ? (P.cellw ? 7 : 8) : 7;
   min_blocks = min(max(min_blocks, 6), 8);
-  if (P.cellw && P.cw_sec) {
-    if (P.n_levels > 1) {
-      if (!P.track_pos)
-        return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7, false, true, true>
-                               : trace_pool_fp64_lean_mg<6, false, true, true>;
-      return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7, true, true, true>
-                             : trace_pool_fp64_lean_mg<6, true, true, true>;
-    }
-    if (!P.track_pos)
-      return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, false, true, true>
-             : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, false, true, true>
-                               : trace_pool_fp64_lean<6, 0, false, false, true, true>;
-    return min_blocks >= 7 ? trace_pool_fp64_lean<7, 0, false, true, true, true>
-                           : trace_pool_fp64_lean<6, 0, false, true, true, true>;
-  }
   if (P.cellw) {
     if (P.n_levels > 1) {
       if (!P.track_pos)
@@ -1662,13 +1576,13 @@ cudaError_t launch_build_iv64(const double* k, const double* ib, int nb, int nq,
   return cudaGetLastError();
 }
 
-cudaError_t launch_build_cell_words(const TraceParams& P, int level, const double* field,
-                                    int64_t n, double scale, uint64_t* out, int* bad,
+cudaError_t launch_build_cell_words(const TraceParams& P, const double* field, int64_t n,
+                                    double scale, uint64_t* out, int* bad,
                                     cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int64_t want = (n + 255) / 256;
   build_cell_words<<<static_cast<unsigned>(want < 8192 ? want : 8192), 256, 0, stream>>>(
-      P, P.lv[level], field, n, scale, out, bad);
+      P, field, n, scale, out, bad);
   return cudaGetLastError();
 }
 
