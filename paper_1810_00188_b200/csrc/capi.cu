@@ -335,7 +335,6 @@ struct Tune {
   int sort_block = 0;  // cubic sort tiles (edge in cells; 0 = linear tiles)
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
   int cellw = 1;       // fp64 lean tracers read precomputed cell words (trace_fp64.cu)
-  int fp64_hint = 0;   // cell-word gathers: 1 L1::no_allocate, 2 evict_first (records evict_last)
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -362,7 +361,6 @@ const Tune& tune() {
     x.sort_dirs = std::max(1, env_int("ERMC_SORT_DIRS", x.sort_dirs));
     x.sort_block = std::max(0, env_int("ERMC_SORT_BLOCK", x.sort_block));
     x.cellw = env_int("ERMC_CELLW", x.cellw);
-    x.fp64_hint = env_int("ERMC_FP64_HINT", x.fp64_hint);
     return x;
   }();
   return t;
@@ -805,7 +803,6 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.refill_threshold = tune().refill;
   P.inner_steps = c.n_levels > 1 ? tune().inner_steps_mg : tune().inner_steps;
   P.lean = tune().lean && s->tables_finite;
-  P.hint = tune().fp64_hint;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;

@@ -74,17 +74,6 @@ __device__ __forceinline__ double ld_t64(const double* p) {
   return r;
 }
 template <int kHint>
-__device__ __forceinline__ uint64_t ld_w64(const uint64_t* p) {
-  uint64_t r;
-  if (kHint == 1)
-    asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(r) : "l"(p));
-  else if (kHint == 2)
-    asm("ld.global.nc.L1::evict_first.u64 %0, [%1];" : "=l"(r) : "l"(p));
-  else
-    r = __ldg(reinterpret_cast<const unsigned long long*>(p));
-  return r;
-}
-template <int kHint>
 __device__ __forceinline__ float4 ld_rec32(const float4* p) {
   if (kHint == 0) return __ldg(p);
   float4 r;

@@ -970,7 +970,7 @@ struct Fp64Lean {
     uint64_t w_next = w_cur;
     if (inside || periodic) {
       if (kCW)
-        w_next = ld_w64<kHint>(L.cellw + nlin);
+        w_next = __ldg(L.cellw + nlin);
       else
         t_next = ld_t64<kHint>((kBrick ? L.field64b : L.field) + nlin);
     }
@@ -1449,13 +1449,10 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
       return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7, true, true>
                              : trace_pool_fp64_lean_mg<6, true, true>;
     }
-    if (!P.track_pos) {
-      if (P.hint == 1 && min_blocks == 7) return trace_pool_fp64_lean<7, 1, false, false, true>;
-      if (P.hint == 2 && min_blocks == 7) return trace_pool_fp64_lean<7, 2, false, false, true>;
+    if (!P.track_pos)
       return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, false, true>
              : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, false, true>
                                : trace_pool_fp64_lean<6, 0, false, false, true>;
-    }
     return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, true, true>
            : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, true, true>
                              : trace_pool_fp64_lean<6, 0, false, true, true>;
