@@ -322,7 +322,6 @@ struct Tune {
   int inner_steps_mg = 48;    // multigrid (n_levels > 1), fp64: measured -1..-4 % time
   int inner_steps32_mg = 64;  // multigrid, fp32: measured -1 %
   int refill = 8;
-  int exit_idle_mg = 16;  // multigrid: idle lanes that end a march window early
   int fp64_min_blocks = 0;  // 0 = per-tracer default (trace_fp64.cu)
   int fp32_min_blocks = 8;
   int lean = 1;
@@ -349,7 +348,6 @@ const Tune& tune() {
     x.inner_steps_mg = std::max(1, env_int("ERMC_INNER_STEPS_MG", x.inner_steps_mg));
     x.inner_steps32_mg = std::max(1, env_int("ERMC_INNER_STEPS32_MG", x.inner_steps32_mg));
     x.refill = std::max(1, std::min(32, env_int("ERMC_REFILL", x.refill)));
-    x.exit_idle_mg = std::max(1, std::min(33, env_int("ERMC_EXIT_IDLE_MG", x.exit_idle_mg)));
     x.fp64_min_blocks = env_int("ERMC_FP64_MINB", x.fp64_min_blocks);
     x.fp32_min_blocks = env_int("ERMC_FP32_MINB", x.fp32_min_blocks);
     x.lean = env_int("ERMC_LEAN", x.lean);
@@ -803,7 +801,6 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.h_seed = mix64_host(c.seed + 0x9e3779b97f4a7c15ULL);
   P.rays = c.rays_per_cell;
   P.refill_threshold = tune().refill;
-  P.exit_idle = tune().exit_idle_mg;
   P.inner_steps = c.n_levels > 1 ? tune().inner_steps_mg : tune().inner_steps;
   P.lean = tune().lean && s->tables_finite;
   P.tol32 = static_cast<float>(c.tolerance);

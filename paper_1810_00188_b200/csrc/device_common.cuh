@@ -319,8 +319,9 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
         pool_next = pool_end;
       }
     }
-    const unsigned active_mask = __ballot_sync(kFullMask, active);
-    if (active_mask == 0u && exhausted && pool_next >= pool_end) break;
+    if (__ballot_sync(kFullMask, active) == 0u && exhausted &&
+        pool_next >= pool_end)
+      break;
     int done_lvl = -1;  // kMulti: final level of a ray that just ended
     uint32_t done_sal = 0;
     if (active) {
@@ -328,18 +329,10 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
       // whose ray ends early idles for < inner_steps iterations.
       int st = kContinue;
       if constexpr (kMulti) {
-        // not unrolled: the demotion makes the step body large (i-cache).
-        // Multigrid rays are short (~22 steps at 7 levels): every 8 steps the
-        // warp checks how many lanes still march and leaves the window once
-        // exit_idle lanes are idle, so they are refilled together (one
-        // converged pass of ray generation) instead of idling to its end.
-        for (int s = 1;; ++s) {
-          if (st == kContinue) st = tr.step(P, max_steps);
-          if ((s & 7) == 0 || s >= P.inner_steps) {
-            const unsigned live = __ballot_sync(active_mask, st == kContinue);
-            if (s >= P.inner_steps || __popc(live) + P.exit_idle <= 32u) break;
-          }
-        }
+        // not unrolled: the demotion makes the step body large (i-cache)
+#pragma unroll 1
+        for (int s = 0; s < P.inner_steps && st == kContinue; ++s)
+          st = tr.step(P, max_steps);
       } else {
 #pragma unroll 2  // measured +0.2 % (fp64) / +0.6 % (fp32)
         for (int s = 0; s < P.inner_steps && st == kContinue; ++s)

@@ -121,7 +121,6 @@ struct TraceParams {
   // ---- work decomposition ----
   int32_t refill_threshold;  // idle lanes before a warp regenerates rays
   int32_t inner_steps;       // march steps between two pool checks
-  int32_t exit_idle;         // multigrid: leave the window early once this many lanes idle
   int32_t lean;              // fp64: 1 = lean tracer (per-axis records in smem)
   int32_t brick;             // lean tracers read the micro-brick field copy
   int32_t track_pos;         // 0 when every wall is black (positions never read)
