@@ -16,7 +16,7 @@ fi
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   NCU=/usr/local/cuda/bin/ncu
   timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
-     --log-file $OUT/ncu_launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-e2e --cpu-seconds 2 > $OUT/ncu_launches_bench_$TAG.json 2>&1
+     --log-file $OUT/ncu_launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > $OUT/ncu_launches_bench_$TAG.json 2>&1
   for P in fp64 fp32; do
     timeout 900 $NCU --set full --clock-control none --import-source on -k regex:trace_pool -s 1 -c 1 \
       -o $OUT/prof_${P}_$TAG -f python bench.py --grid 256 --rays 16 --precision $P --steps 1 --warmup 1 \

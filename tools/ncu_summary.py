@@ -109,7 +109,13 @@ def main():
             summary[prec].update(l2_bytes_per_step=l2 / steps, l2_gb_per_s=l2 / (ms * 1e-3) / 1e9,
                                  dram_gb_per_s=dram / (ms * 1e-3) / 1e9,
                                  thread_efficiency=float(m[
-                                     "smsp__thread_inst_executed_per_inst_executed.ratio"][0]) / 32)
+                                     "smsp__thread_inst_executed_per_inst_executed.ratio"][0]) / 32,
+                                 lts_throughput_pct=float(m[
+                                     "lts__throughput.avg.pct_of_peak_sustained_elapsed"][0]),
+                                 lsu_wavefronts_pct=float(m[
+                                     "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"][0]),
+                                 thread_inst_per_step=float(m["smsp__inst_executed.sum"][0].replace(",", "")) *
+                                 float(m["smsp__thread_inst_executed_per_inst_executed.ratio"][0]) / steps)
     summary_path.write_text(json.dumps(summary, indent=1) + "\n")
     print(json.dumps(summary, indent=1))
 
