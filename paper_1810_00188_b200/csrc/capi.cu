@@ -335,7 +335,6 @@ struct Tune {
   int sort_block = 0;  // cubic sort tiles (edge in cells; 0 = linear tiles)
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
   int cellw = 1;       // fp64 lean tracers read precomputed cell words (trace_fp64.cu)
-  int pipe = 1;        // ... software-pipelined for black-wall single-level solves
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -362,7 +361,6 @@ const Tune& tune() {
     x.sort_dirs = std::max(1, env_int("ERMC_SORT_DIRS", x.sort_dirs));
     x.sort_block = std::max(0, env_int("ERMC_SORT_BLOCK", x.sort_block));
     x.cellw = env_int("ERMC_CELLW", x.cellw);
-    x.pipe = env_int("ERMC_PIPE", x.pipe);
     return x;
   }();
   return t;
@@ -955,7 +953,6 @@ void ensure_cell_words(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
   if (!s->cellw_ok) return;
   for (size_t l = 0; l < s->d_cellw.size(); ++l) P.lv[l].cellw = s->d_cellw[l]->p;
   P.cellw = 1;
-  P.pipe = tune().pipe && P.n_levels == 1 && !P.track_pos ? 1 : 0;
 }
 
 // Core solve of [lo, hi) into device outputs.

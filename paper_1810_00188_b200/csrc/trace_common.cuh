@@ -94,7 +94,6 @@ struct TraceParams {
   // cw_rdt = RN(1 / cw_dt) (Markstein: the reference's RN((T - t[lo]) / dt),
   // bitwise; the builder checks it cell by cell).
   int32_t cellw;             // 1: the lean fp64 tracers read cell words
-  int32_t pipe;              // 1: black-wall single-level solves use Fp64Pipe
   int32_t cw_shift;          // lo = w >> cw_shift (64 - bits of the interval index)
   double cw_dt, cw_rdt;
 

@@ -1089,171 +1089,6 @@ struct Fp64Lean {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-// Software-pipelined cell-word tracer for single-level solves with black
-// walls (the BASELINE configs). Same operations and rounding as Fp64Lean
-// (hence the reference), reordered across iterations so that no gather sits
-// on a step's critical path. The DDA never depends on absorption
-// (tracer.cpp:103-129), so within step s:
-//   1. the word of cell s+1 (requested during step s-1) selects its interval
-//      record, requested now — it is consumed by step s+1's absorption;
-//   2. the DDA decides the crossing that ends step s+1 and requests the word
-//      of the cell it enters (cell s+2);
-//   3. cell s absorbs, with the record requested during step s-1.
-// State at the start of step s: ds / `wall` of step s, the record `v` and
-// `frac` of cell s, the word `w1` of cell s+1, and tn, the per-axis records
-// and `lin1` advanced past step s's crossing. A wall ends the ray (black
-// walls: tau *= 1 - 1), so there is no reflection state.
-struct Fp64Pipe {
-  double tn[3];
-  double tau, q, last_ib2, ib1, rib1, pref;
-  double4 v;       // interval record of the current cell
-  double frac;     // the current cell's interpolation weight
-  double ds;       // the current step's path length
-  uint64_t w1;     // the next cell's word
-  int4* ax;
-  int row, lin1, steps_;
-  int wall;        // face (2 axis + hi) the current step ends on, or -1
-  int err;
-
-  // Dda::setup (tracer.cpp:17-38) into tn / the per-axis records.
-  __device__ __forceinline__ void setup(const LevelDesc& L, const Ray& r) {
-    const int stride[3] = {L.n[1] * L.n[2], L.n[2], 1};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double da = r.dir[a];
-      if (da == 0.0) {
-        tn[a] = __longlong_as_double(0x7ff0000000000000LL);
-        ax[a * kBlock] = make_int4(0, 0x7ff00000, 0, r.idx[a]);
-        continue;
-      }
-      const bool pos_dir = da > 0.0;
-      const int face_idx = r.idx[a] + (pos_dir ? 1 : 0);
-      const double face = L.origin[a] + face_idx * L.d[a];
-      const double rda = 1.0 / da;
-      tn[a] = div_rcp(face - r.pos[a], da, rda);
-      const double td = div_rcp(L.d[a], fabs(da), fabs(rda));
-      ax[a * kBlock] = make_int4(__double2loint(td), __double2hiint(td),
-                                 pos_dir ? stride[a] : -stride[a],
-                                 pos_dir ? L.n[a] - 1 - r.idx[a] : r.idx[a]);
-    }
-  }
-
-  // The DDA of one step (tracer.cpp:103-129, the index update of :139-153):
-  // returns its length, sets `face` to the wall it ends on (or -1) and
-  // otherwise lin1 / w1 to the cell it enters (the word requested now);
-  // tn advances past the crossing.
-  __device__ __forceinline__ double dda_ahead(const TraceParams& P, const LevelDesc& L,
-                                              int& face) {
-    int axis = 0;
-    double d = tn[0];
-    if (tn[1] < d) {
-      d = tn[1];
-      axis = 1;
-    }
-    if (tn[2] < d) {
-      d = tn[2];
-      axis = 2;
-    }
-    if (d < 0.0) d = 0.0;
-    int4* rp = ax + axis * kBlock;
-    const int4 rec = *rp;
-    const double td = __hiloint2double(rec.y, rec.x);
-    const int left = rec.w - 1;
-    const bool inside = left >= 0;
-    const bool periodic = (P.periodic_mask >> axis) & 1;
-    int nlin = lin1 + rec.z;
-    if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
-    const double advance = d + L.eps;
-    tn[0] -= advance;
-    tn[1] -= advance;
-    tn[2] -= advance;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-      if (a == axis) tn[a] += td;
-    if (inside || periodic) {
-      w1 = __ldg(L.cellw + nlin);
-      rp->w = inside ? left : L.n[axis] - 1;
-      lin1 = nlin;
-      face = -1;
-    } else {
-      face = 2 * axis + (rec.z > 0 ? 1 : 0);
-    }
-    return d;
-  }
-
-  __device__ __forceinline__ int init(const TraceParams& P, int64_t cell, uint32_t ray) {
-    extern __shared__ int4 s_dyn[];
-    ax = s_dyn + threadIdx.x;
-    Ray r;
-    const double* cdf =
-        P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock) : nullptr;
-    const int e = init_ray<true, true>(P, cell, ray, r, nullptr, cdf);
-    if (e != kErrNone) return e;
-    const LevelDesc& L = P.lv[0];
-    tau = 1.0;
-    q = 0.0;
-    ib1 = r.ib1;
-    last_ib2 = r.ib1;
-    rib1 = 1.0 / r.ib1;
-    pref = r.pref;
-    row = (r.band * P.n_quad + r.quad) * (P.n_temps - 1);
-    steps_ = 0;
-    ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw), static_cast<int>(cell),
-                               static_cast<int>(ray));
-    int lo;
-    decode_cw(P, __ldg(L.cellw + cell), lo, frac);  // the source cell (L1 hit: init_ray read it)
-    v = ld_rec64<0>(P.iv64 + row + lo);
-    setup(L, r);
-    lin1 = static_cast<int>(cell);
-    ds = dda_ahead(P, L, wall);  // step 0's crossing, cell 1's word
-    return kErrNone;
-  }
-
-  __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
-    if (tau <= P.tol) return kDone;
-    if (steps_ >= max_steps) return kDone;
-    const LevelDesc& L = P.lv[0];
-    double4 v1 = v;
-    double frac1 = frac, ds1 = 0.0;
-    int wall1 = -1;
-    if (wall < 0) {
-      int lo;
-      decode_cw(P, w1, lo, frac1);               // 1. cell s+1's record ...
-      v1 = ld_rec64<0>(P.iv64 + row + lo);
-      ds1 = dda_ahead(P, L, wall1);               // 2. ... step s+1's crossing
-    }
-    // 3. absorption in the current cell (tracer.cpp:115-122)
-    const double kappa = v.x + frac * (v.y - v.x);
-    const double ib2 = v.z + frac * (v.w - v.z);
-    const double alpha = -expm1_lean(-kappa * ds);
-    last_ib2 = ib2;
-    q += P.qe * tau * alpha * div_rcp(ib2 - ib1, ib1, rib1) * pref;
-    tau *= 1.0 - alpha;
-    ++steps_;
-    if (wall >= 0) {  // wall exchange (tracer.cpp:155-163); black: the ray ends
-      const int4 r3 = ax[3 * kBlock];
-      const double ew = P.wall_eps[wall];
-      const double ib_w = __ldg(P.wall_ib + wall * P.n_bands + r3.x);
-      q += P.qe * tau * ew * div_rcp(ib_w - ib1, ib1, rib1) * pref;
-      tau *= 1.0 - ew;
-      return kDone;
-    }
-    v = v1;
-    frac = frac1;
-    ds = ds1;
-    wall = wall1;
-    return kContinue;
-  }
-
-  __device__ __forceinline__ double finish(const TraceParams& P) const {
-    return q + P.qe * tau * div_rcp(last_ib2 - ib1, ib1, rib1) * pref;
-  }
-  __device__ __forceinline__ bool finite_state() const { return isfinite(tau); }
-  __device__ __forceinline__ int level() const { return 0; }
-  __device__ __forceinline__ int sal() const { return steps_; }
-  __device__ __forceinline__ int steps() const { return steps_; }
-};
-
 struct Fp64Tracer {
   Ray r;
   int err;
@@ -1301,15 +1136,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
   extern __shared__ int4 s_dyn[];
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
-}
-
-// The software-pipelined black-wall cell-word tracer (single level).
-template <int kMinBlocks>
-__global__ void __launch_bounds__(kBlock, kMinBlocks)
-    trace_pool_fp64_pipe(const __grid_constant__ TraceParams P) {
-  extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
-  pool_kernel_body<Fp64Pipe, false>(P);
 }
 
 // Multigrid variant of the lean tracer (n_levels > 1).
@@ -1623,8 +1449,6 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
       return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7, true, true>
                              : trace_pool_fp64_lean_mg<6, true, true>;
     }
-    if (!P.track_pos && P.pipe)
-      return min_blocks >= 7 ? trace_pool_fp64_pipe<7> : trace_pool_fp64_pipe<6>;
     if (!P.track_pos)
       return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, false, true>
              : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, false, true>
