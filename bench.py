@@ -141,14 +141,24 @@ class ClockSampler:
                 rows.append(f)
         if not rows:
             return None
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
+        pw = [num(r[2]) for r in rows if num(r[2]) is not None]
         load = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        busy = [p for p in pw if p > 0.5 * (max(pw) if pw else 1)]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        capped = sum(1 for r in rows if r[7] == "Active")
         return {"sm_mhz": statistics.median(load) if load else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "sw_power_cap_samples": capped,
+                "power_w_median": statistics.median(busy) if busy else None,
+                "power_w_max": max(pw) if pw else None}
 
 
 # ----------------------------------------------------------------- shared
