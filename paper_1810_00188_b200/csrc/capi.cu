@@ -910,12 +910,6 @@ void ensure_cell_words(ermc_session* s, ermc_dev::TraceParams& P, cudaStream_t s
   if (!tune().cellw || !P.lean || P.brick || !P.tint_arith || v.nt < 2 || v.nt - 1 > 256 ||
       !(v.temps[0] > 0.0))
     return;
-  // the cell-word tracers pack stride and cells left in one int per axis
-  // (trace_fp64.cu kLeftBits): at most 2047 cells per axis, |stride| < 2^20
-  for (const ermc_grid_t& g : s->level_grids)
-    if (g.nx > 2047 || g.ny > 2047 || g.nz > 2047 ||
-        static_cast<int64_t>(g.ny) * g.nz >= (int64_t(1) << 20))
-      return;
   int e = 0;
   std::frexp(v.temps[0], &e);              // t_first = f 2^e, f in [0.5, 1)
   const double scale = std::ldexp(1.0, 52 - (e - 1));  // 1 / ulp(t_first)

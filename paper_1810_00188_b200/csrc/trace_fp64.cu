@@ -787,15 +787,6 @@ __device__ __forceinline__ double expm1_lean(double x) {
 // position, `locate`d as in geometry.cpp:112-138; the per-axis records and
 // the field pointer are then the coarse level's.
 constexpr int kLeanRecs64 = 4;
-// kCW tracers pack the per-axis records tighter (fewer shared-memory
-// wavefronts per step): t_delta[3] as doubles, then one int per axis
-// (signed stride << kLeftBits | cells left), then the int4 wall record —
-// a step reads 8 + 4 bytes and writes 4 contiguous bytes instead of
-// reading 16 and writing 4 at a 16-byte stride (a 4-way conflict).
-constexpr int kLeftBits = 11, kLeftMask = (1 << kLeftBits) - 1;
-constexpr int kPackTdInt4 = 3 * 8 * kBlock / 16;           // 192
-constexpr int kPackR3Int4 = kPackTdInt4 + 3 * 4 * kBlock / 16;  // 288
-constexpr int kPackInt4 = kPackR3Int4 + kBlock;            // 416 int4 = 6656 B
 
 // kReflect = false (every wall black) drops the reflection code; the
 // multigrid tracer keeps positions for demotion but can still drop it.
@@ -811,16 +802,14 @@ struct Fp64Lean {
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
   uint64_t w_cur;  // kCW: the current cell's word
-  int4* ax;        // !kCW: per-axis int4 records; kCW: the wall record
-  double* axd;     // kCW: t_delta per axis
-  int* axs;        // kCW: packed stride / cells left per axis
+  int4* ax;
   int row;  // first interval record of (band, g) in iv64
   int lin, steps_;
   int lvl, sal_;  // kMulti: current level, steps on it
   int err;
 
   __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
-    const int left = kCW ? (axs[a * kBlock] & kLeftMask) : ax[a * kBlock].w;
+    const int left = ax[a * kBlock].w;
     if (dir[a] == 0.0) return left;
     return dir[a] > 0.0 ? L.n[a] - 1 - left : left;
   }
@@ -835,12 +824,7 @@ struct Fp64Lean {
       const double da = dir[a];
       if (da == 0.0) {
         tn[a] = __longlong_as_double(0x7ff0000000000000LL);
-        if (kCW) {
-          axd[a * kBlock] = __longlong_as_double(0x7ff0000000000000LL);
-          axs[a * kBlock] = idx[a];
-        } else {
-          ax[a * kBlock] = make_int4(0, 0x7ff00000, 0, idx[a]);
-        }
+        ax[a * kBlock] = make_int4(0, 0x7ff00000, 0, idx[a]);
         continue;
       }
       const bool pos_dir = da > 0.0;
@@ -852,16 +836,9 @@ struct Fp64Lean {
       const double rda = 1.0 / da;
       tn[a] = div_rcp(face - pos[a], da, rda);
       const double td = div_rcp(L.d[a], fabs(da), fabs(rda));
-      if (kCW) {
-        axd[a * kBlock] = td;
-        axs[a * kBlock] = static_cast<int>(static_cast<unsigned>(pos_dir ? stride[a] : -stride[a])
-                                           << kLeftBits) |
-                          (pos_dir ? L.n[a] - 1 - idx[a] : idx[a]);
-      } else {
-        ax[a * kBlock] = make_int4(__double2loint(td), __double2hiint(td),
-                                   pos_dir ? stride[a] : -stride[a],
-                                   pos_dir ? L.n[a] - 1 - idx[a] : idx[a]);
-      }
+      ax[a * kBlock] = make_int4(__double2loint(td), __double2hiint(td),
+                                 pos_dir ? stride[a] : -stride[a],
+                                 pos_dir ? L.n[a] - 1 - idx[a] : idx[a]);
     }
     lin = kBrick ? brick_index(L, idx[0], idx[1], idx[2])
                  : (idx[0] * L.n[1] + idx[1]) * L.n[2] + idx[2];
@@ -870,17 +847,10 @@ struct Fp64Lean {
   __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
                                       uint32_t ray) {
     extern __shared__ int4 s_dyn[];
-    if (kCW) {
-      axd = reinterpret_cast<double*>(s_dyn) + threadIdx.x;
-      axs = reinterpret_cast<int*>(s_dyn + kPackTdInt4) + threadIdx.x;
-      ax = s_dyn + kPackR3Int4 + threadIdx.x - 3 * kBlock;  // ax[3 * kBlock]: the wall record
-    } else {
-      ax = s_dyn + threadIdx.x;
-    }
+    ax = s_dyn + threadIdx.x;
     Ray r;
     const double* cdf =
-        P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + (kCW ? kPackInt4 : kLeanRecs64 * kBlock))
-                   : nullptr;
+        P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock) : nullptr;
     const int e = init_ray<true, kCW>(P, cell, ray, r, nullptr, cdf);
     if (e != kErrNone) return e;
 #pragma unroll
@@ -976,18 +946,8 @@ struct Fp64Lean {
     if (ds < 0.0) ds = 0.0;
 
     int4* rp = ax + axis * kBlock;
-    int4 rec;
-    int* sp = nullptr;
-    int sl = 0;
-    if (kCW) {  // packed records: rec = {-, -, stride, cells left}
-      sp = axs + axis * kBlock;
-      sl = *sp;
-      rec.z = sl >> kLeftBits;
-      rec.w = sl & kLeftMask;
-    } else {
-      rec = *rp;
-    }
-    const double td = kCW ? axd[axis * kBlock] : __hiloint2double(rec.y, rec.x);
+    const int4 rec = *rp;
+    const double td = __hiloint2double(rec.y, rec.x);
     const int left = rec.w - 1;
     const bool inside = left >= 0;
     const bool periodic = (P.periodic_mask >> axis) & 1;
@@ -1042,20 +1002,14 @@ struct Fp64Lean {
     if (kMulti) ++sal_;
 
     if (inside) {
-      if (kCW)
-        *sp = sl - 1;
-      else
-        rp->w = left;
+      rp->w = left;
       lin = nlin;
       t_cur = t_next;
       w_cur = w_next;
       return kContinue;
     }
     if (periodic) {
-      if (kCW)
-        *sp = (sl & ~kLeftMask) | (L.n[axis] - 1);
-      else
-        rp->w = L.n[axis] - 1;
+      rp->w = L.n[axis] - 1;
       const double ext = L.extent[axis];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
@@ -1180,8 +1134,7 @@ template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = f
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem)
-    stage_cdfs(P, reinterpret_cast<double*>(s_dyn + (kCW ? kPackInt4 : kLeanRecs64 * kBlock)));
+  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
 }
 
@@ -1190,8 +1143,7 @@ template <int kMinBlocks, bool kReflect = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem)
-    stage_cdfs(P, reinterpret_cast<double*>(s_dyn + (kCW ? kPackInt4 : kLeanRecs64 * kBlock)));
+  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
 }
 
@@ -1472,7 +1424,7 @@ bool lean_path(const TraceParams& P) {
 }
 size_t fp64_smem(const TraceParams& P) {
   if (!lean_path(P)) return 0;
-  return (P.cellw ? static_cast<size_t>(kPackInt4) : kLeanRecs64 * kBlock) * sizeof(int4) +
+  return kLeanRecs64 * kBlock * sizeof(int4) +
          (P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad) : 0);
 }
 // min_blocks = 0 picks the measured best per variant (B200, 256^3 channel):
