@@ -767,81 +767,6 @@ __device__ __forceinline__ double expm1_lean(double x) {
   return fma(sc, e, sc - 1.0);
 }
 
-// expm1 by a 32-entry table: x = (32 k + i) ln2/32 + r, i in [-16, 15] (so
-// k = 0 for |x| < ln2/2 and no cancellation in the reconstruction),
-// |r| <= ln2/64, e^r - 1 by its degree-7 Taylor polynomial (truncation
-// < 1e-18 relative), expm1(x) = 2^k (T_i (e^r - 1) + (T_i - 1)) + (2^k - 1)
-// with T_i = RN(2^(i/32)) and T_i - 1 rounded separately (an exact
-// decimal evaluation, not T_i - 1 in double). 6 polynomial FMAs instead of
-// 12 and one shared-memory read of {T_i, T_i - 1}. Within 1 ulp of glibc's
-// expm1 on x <= 0 (the march's -kappa ds), the same bound as expm1_lean
-// (tests/test_oracle.py::test_expm1_table_restatement).
-__constant__ double2 kEmTab[32] = {
-    {0.7071067811865476, -0.2928932188134525},
-    {0.7225904034885233, -0.2774095965114767},
-    {0.7384130729697497, -0.2615869270302503},
-    {0.7545822137967114, -0.24541778620328863},
-    {0.7711054127039704, -0.2288945872960296},
-    {0.7879904225539432, -0.21200957744605675},
-    {0.8052451659746271, -0.19475483402537286},
-    {0.8228777390769825, -0.17712226092301758},
-    {0.8408964152537145, -0.15910358474628547},
-    {0.859309649061239, -0.14069035093876103},
-    {0.8781260801866497, -0.12187391981335026},
-    {0.8973545375015536, -0.1026454624984464},
-    {0.9170040432046712, -0.08299595679532877},
-    {0.93708381705515, -0.06291618294485005},
-    {0.9576032806985737, -0.042396719301426355},
-    {0.9785720620877001, -0.021427937912299865},
-    {1.0, 0.0},
-    {1.0218971486541166, 0.02189714865411668},
-    {1.0442737824274138, 0.04427378242741384},
-    {1.0671404006768237, 0.06714040067682361},
-    {1.0905077326652577, 0.09050773266525766},
-    {1.1143867425958924, 0.11438674259589254},
-    {1.1387886347566916, 0.13878863475669165},
-    {1.1637248587775775, 0.1637248587775775},
-    {1.189207115002721, 0.18920711500272105},
-    {1.215247359980469, 0.21524735998046887},
-    {1.241857812073484, 0.24185781207348406},
-    {1.2690509571917332, 0.2690509571917332},
-    {1.2968395546510096, 0.29683955465100964},
-    {1.3252366431597413, 0.32523664315974127},
-    {1.3542555469368927, 0.3542555469368927},
-    {1.383909881963832, 0.38390988196383197}};
-__shared__ double2 s_em_tab[32];
-
-// Every lean fp64 kernel stages the table before its pool starts.
-__device__ __forceinline__ void stage_em_table() {
-  if (threadIdx.x < 32) s_em_tab[threadIdx.x] = kEmTab[threadIdx.x];
-  __syncthreads();
-}
-
-__device__ __forceinline__ double expm1_tab(double x) {
-  if (!(x >= -40.0 && x <= 0.5)) {
-    if (x < -40.0) return -1.0;  // |expm1(x) + 1| < 2^-57
-    return expm1(x);             // NaN, positive arguments: libdevice
-  }
-  const double magic = 6755399441055744.0;  // 1.5 * 2^52
-  const double t = fma(x, 46.16624130844683, magic);  // RN(32 / ln2)
-  const double j = t - magic;
-  double r = fma(j, -6.93147180369123816490e-01 / 32, x);  // fdlibm's ln2 split / 32
-  r = fma(j, -1.90821492927058770002e-10 / 32, r);
-  const int ji = __double2loint(t);
-  const int k = (ji + 16) >> 5;
-  const double2 T = s_em_tab[(ji + 16) & 31];
-  double p = fma(r, 1.0 / 5040, 1.0 / 720);
-  p = fma(p, r, 1.0 / 120);
-  p = fma(p, r, 1.0 / 24);
-  p = fma(p, r, 1.0 / 6);
-  p = fma(p, r, 0.5);
-  const double e = fma(r * r, p, r);
-  const double inner = fma(T.x, e, T.y);
-  if (k == 0) return inner;
-  const double sc = __hiloint2double((k + 1023) << 20, 0);
-  return fma(sc, inner, sc - 1.0);
-}
-
 // Lean single-level fp64 tracer: Fp64Fast's arithmetic (hence the
 // reference's) with the per-axis DDA constants in a per-thread shared-memory
 // record indexed by the stepping axis:
@@ -1056,7 +981,7 @@ struct Fp64Lean {
     // are re-traced by the reference-order debug tracer for the error).
     const double kappa = v.x + frac * (v.y - v.x);
     const double ib2 = v.z + frac * (v.w - v.z);
-    const double alpha = -expm1_tab(-kappa * ds);
+    const double alpha = -expm1_lean(-kappa * ds);
     last_ib2 = ib2;
     q += P.qe * tau * alpha * div_rcp(ib2 - ib1, ib1, rib1) * pref;
     tau *= 1.0 - alpha;
@@ -1209,7 +1134,6 @@ template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = f
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  stage_em_table();
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
 }
@@ -1219,7 +1143,6 @@ template <int kMinBlocks, bool kReflect = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  stage_em_table();
   if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
 }
