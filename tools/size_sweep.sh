@@ -4,7 +4,7 @@
 OUT=gpurun_out; mkdir -p $OUT; TAG=${1:-sz}
 for N in ${SIZES:-64 128 192 256 320 384}; do for P in fp64 fp32; do
   F=$OUT/size_${TAG}_${N}_$P.json
-  timeout 900 python bench.py --grid $N --precision $P --steps 1 --warmup 1 --no-e2e --no-fp32-extra --cpu-seconds 1 > $F 2>&1
+  timeout 900 python bench.py --grid $N --precision $P --steps 1 --warmup 1 --no-e2e --no-fp32-extra --no-cpu --no-parity > $F 2>&1
   python -c "
 import json
 d=json.loads(open('$F').read().splitlines()[-1]); print($N, '$P', '%.4g'%d['value'], round(d['roofline']['frac'],3), round(d['ms_per_step'],1), round(d['steps_per_ray'],1))"
