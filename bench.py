@@ -40,7 +40,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import signal
 import statistics
@@ -75,13 +74,11 @@ def parse():
                    help="channel wall emissivity (1 = config 4's black walls)")
     p.add_argument("--no-fp32-extra", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--ref-rays", type=int, default=1,
                    help="rays per cell of each reference-arm sample solve (whole field)")
     p.add_argument("--no-parity", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-single-worker", action="store_true")
-    p.add_argument("--json-only", action="store_true", help=argparse.SUPPRESS)
     return p.parse_args()
 
 

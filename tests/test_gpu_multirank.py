@@ -38,7 +38,7 @@ def test_fused_gather_is_byte_identical(world, precision):
 @pytest.mark.parametrize("gather", ["fused", "nccl"])
 def test_bench_multirank_flow(gather):
     r = _torchrun(2, ["bench.py", "--gpus", "2", "--steps", "1", "--warmup", "1", "--grid", "64",
-                      "--rays", "8", "--no-e2e", "--cpu-seconds", "1"],
+                      "--rays", "8", "--no-e2e", "--no-cpu"],
                   29610 + (gather == "fused"),
                   env={"ERMC_BENCH_BACKEND": "gloo", "ERMC_BENCH_GATHER": gather})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
