@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(kSortBlock)
                  uint32_t* __restrict__ perm) {
   extern __shared__ __align__(8) unsigned char s_raw[];
   double* s_cdf = reinterpret_cast<double*>(s_raw);
-  unsigned int* s_cur = reinterpret_cast<unsigned int*>(s_raw + cdf_len * sizeof(double));
+  unsigned int* s_cur = reinterpret_cast<unsigned int*>(
+      s_raw + (cdf_len && P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad)
+                                     : cdf_len * sizeof(double)));
   unsigned int* s_part = s_cur + n_bins;
   const uint32_t n = static_cast<uint32_t>(P.n_work);
   const uint32_t rays = static_cast<uint32_t>(P.rays);
@@ -131,22 +133,35 @@ __global__ void __launch_bounds__(kSortBlock)
   const uint32_t cnt = tm.count(n);
   const int nb = P.n_bands, nq = P.n_quad;
   for (int b = threadIdx.x; b < n_bins; b += blockDim.x) s_cur[b] = 0u;
+  // the staged CDFs carry their guide tables (trace kernels' layout) when
+  // the session built them (P.cdf_smem)
+  const bool guided = cdf_len && P.cdf_smem;
   for (int b = threadIdx.x; b < cdf_len; b += blockDim.x)
     s_cdf[b] = b < nb ? P.band_cdf[b] : P.quad_cdf[b - nb];
+  if (guided) {
+    uint8_t* gdst = reinterpret_cast<uint8_t*>(s_cdf + cdf_len);
+    for (int i = threadIdx.x; i < kGuideBand + nb * kGuideQuad; i += blockDim.x)
+      gdst[i] = P.cdf_guide[i];
+  }
   __syncthreads();
   const double* band_cdf = cdf_len ? s_cdf : P.band_cdf;
   const double* quad_cdf = cdf_len ? s_cdf + nb : P.quad_cdf;
   for (uint32_t u = threadIdx.x; u < cnt; u += blockDim.x) {
     const uint32_t w = tm.work(u, n);
     // sample_band on draws 2 and 3 of the ray's key (sampling.cpp:42-53, 77-78)
-    const uint32_t c = w / rays;
+    const uint32_t c = fdiv(w, P.div_rays);
     const uint32_t ray = w - c * rays;
     const uint64_t h_cell =
         mix64(P.h_seed ^ static_cast<uint64_t>(P.cell_base + static_cast<int64_t>(c)));
-    int bn = upper_bound_any(band_cdf, nb, draw_u(h_cell, ray, 2));
-    if (bn >= nb) bn = nb - 1;
-    int g = upper_bound_any(quad_cdf + bn * nq, nq, draw_u(h_cell, ray, 3));
-    if (g >= nq) g = nq - 1;
+    int bn, g;
+    if (guided) {
+      sample_band_cdf(P, s_cdf, draw_u(h_cell, ray, 2), draw_u(h_cell, ray, 3), bn, g);
+    } else {
+      bn = upper_bound_any(band_cdf, nb, draw_u(h_cell, ray, 2));
+      if (bn >= nb) bn = nb - 1;
+      g = upper_bound_any(quad_cdf + bn * nq, nq, draw_u(h_cell, ray, 3));
+      if (g >= nq) g = nq - 1;
+    }
     unsigned key = static_cast<unsigned>(__ldg(row_rank + bn * nq + g));
     if (dir_bins > 1) {
       // Direction bin from draws 0 and 1 (sampling.cpp:31-40): cos(theta) =
@@ -223,7 +238,9 @@ cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_
   }
   const int cdf_total = P.n_bands + P.n_bands * P.n_quad;
   const int cdf_len = cdf_total <= 4096 ? cdf_total : 0;
-  const size_t smem = cdf_len * sizeof(double) + (n_bins + kSortBlock) * sizeof(unsigned int);
+  const size_t cdf_bytes = cdf_len && P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad)
+                                                 : cdf_len * sizeof(double);
+  const size_t smem = cdf_bytes + (n_bins + kSortBlock) * sizeof(unsigned int);
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(
         ng_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
