@@ -52,3 +52,18 @@ def test_reference_arm_is_reference_only_and_same_config(model):
     a = A()
     a.model = model
     assert line["config"] == bench.config_dict(a, 1, hashes)
+
+
+def test_gpus_flag_spawns_ranks_without_a_launcher():
+    # `bench.py --gpus 2` with no WORLD_SIZE: bench.py starts both ranks
+    # itself (the driver's N > 1 invocation works with or without torchrun);
+    # on the reference arm rank 0 alone runs and prints one line.
+    import os
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                        "--grid", "16", "--rays", "8", "--steps", "1", "--warmup", "0",
+                        "--no-single-worker"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
