@@ -335,6 +335,7 @@ struct Tune {
   int sort_block = 0;  // cubic sort tiles (edge in cells; 0 = linear tiles)
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
   int cellw = 1;       // fp64 lean tracers read precomputed cell words (trace_fp64.cu)
+  int carveout = 0;    // trace kernels: smallest shared-memory carveout (-1 driver default)
 };
 int env_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
@@ -361,6 +362,7 @@ const Tune& tune() {
     x.sort_dirs = std::max(1, env_int("ERMC_SORT_DIRS", x.sort_dirs));
     x.sort_block = std::max(0, env_int("ERMC_SORT_BLOCK", x.sort_block));
     x.cellw = env_int("ERMC_CELLW", x.cellw);
+    x.carveout = env_int("ERMC_CARVEOUT", x.carveout);
     return x;
   }();
   return t;
@@ -803,6 +805,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.refill_threshold = tune().refill;
   P.inner_steps = c.n_levels > 1 ? tune().inner_steps_mg : tune().inner_steps;
   P.lean = tune().lean && s->tables_finite;
+  P.carveout = tune().carveout;
   P.tol32 = static_cast<float>(c.tolerance);
   P.tint = s->d_tint.p;
   P.iv64 = s->d_iv64.p;

@@ -93,6 +93,8 @@ struct TraceParams {
   // cell once per field. frac = RN(m / cw_dt) with cw_dt = dt * 2^s and
   // cw_rdt = RN(1 / cw_dt) (Markstein: the reference's RN((T - t[lo]) / dt),
   // bitwise; the builder checks it cell by cell).
+  int32_t carveout;          // shared-memory carveout request: -1 driver default,
+                             // 0 the smallest that holds the resident blocks, > 0 percent
   int32_t cellw;             // 1: the lean fp64 tracers read cell words
   int32_t cw_shift;          // lo = w >> cw_shift (64 - bits of the interval index)
   double cw_dt, cw_rdt;
@@ -158,5 +160,30 @@ struct RayRecord {
   int32_t err_axis;
   int32_t pad;
 };
+
+#ifdef __CUDACC__
+// L1 / shared-memory split of a trace kernel. The driver's default for these
+// kernels is the 132 KB shared-memory configuration (ncu
+// launch__shared_mem_config_size), although their resident blocks need far
+// less: the smallest configuration that holds `blocks` blocks (their dynamic
+// and static shared memory plus the 1 KB the driver reserves per block)
+// leaves the rest of the 256 KB to the L1 that caches the gathers.
+inline cudaError_t set_trace_carveout(const void* fn, int grid, size_t dyn_smem, int request) {
+  if (request < 0) return cudaSuccess;
+  int pct = request;
+  if (pct == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, fn);
+    const int blocks = (grid + sms - 1) / sms;
+    const size_t need = static_cast<size_t>(blocks) * (dyn_smem + fa.sharedSizeBytes + 1024);
+    pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+    if (pct > 100) pct = 100;
+  }
+  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+#endif
 
 }  // namespace ermc_dev

@@ -921,7 +921,9 @@ int trace_fp32_blocks_per_sm(const TraceParams& P, int min_blocks) {
 
 cudaError_t launch_trace_fp32(const TraceParams& P, int grid, int min_blocks,
                               cudaStream_t stream) {
-  fp32_kernel(P, min_blocks)<<<grid, kBlock32, fp32_smem(P), stream>>>(P);
+  const auto k = fp32_kernel(P, min_blocks);
+  set_trace_carveout(reinterpret_cast<const void*>(k), grid, fp32_smem(P), P.carveout);
+  k<<<grid, kBlock32, fp32_smem(P), stream>>>(P);
   return cudaGetLastError();
 }
 

@@ -1498,6 +1498,7 @@ cudaError_t launch_trace_fp64(const TraceParams& P, int grid, int min_blocks,
                               cudaStream_t stream) {
   TraceFn k = fp64_kernel_p(P, min_blocks);
   if (!k) k = fp64_kernel(!fp64_fast_path(P), min_blocks);
+  set_trace_carveout(reinterpret_cast<const void*>(k), grid, fp64_smem(P), P.carveout);
   k<<<grid, kBlock, fp64_smem(P), stream>>>(P);
   return cudaGetLastError();
 }
