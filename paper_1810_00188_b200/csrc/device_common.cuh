@@ -184,6 +184,27 @@ __device__ __forceinline__ void sample_band_cdf(const TraceParams& P, const doub
   if (g >= nq) g = nq - 1;
 }
 
+// The same with only the guide tables staged (in shared memory) and the
+// CDF values read through the read-only path (L1): the lean black-wall
+// tracers keep their shared memory small enough for a 64 KB carveout.
+__device__ __forceinline__ void sample_band_guided(const TraceParams& P, const uint8_t* guide,
+                                                   double r_n, double r_g, int& n, int& g) {
+  const int nb = P.n_bands, nq = P.n_quad;
+  n = guide[static_cast<int>(r_n * kGuideBand)];
+  while (n < nb && !(r_n < __ldg(P.band_cdf + n))) ++n;
+  if (n >= nb) n = nb - 1;
+  const double* qc = P.quad_cdf + n * nq;
+  g = guide[kGuideBand + n * kGuideQuad + static_cast<int>(r_g * kGuideQuad)];
+  while (g < nq && !(r_g < __ldg(qc + g))) ++g;
+  if (g >= nq) g = nq - 1;
+}
+
+__device__ __forceinline__ void stage_guides(const TraceParams& P, uint8_t* dst) {
+  for (int i = threadIdx.x; i < kGuideBand + P.n_bands * kGuideQuad; i += blockDim.x)
+    dst[i] = P.cdf_guide[i];
+  __syncthreads();
+}
+
 // sample_band (reference sampling.cpp:42-53).
 __device__ __forceinline__ void sample_band(const TraceParams& P, double r_n,
                                             double r_g, int& n, int& g) {

@@ -437,7 +437,8 @@ template <bool kLean = false, bool kCW = false>
 __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
                                         uint32_t ray_id, Ray& r,
                                         const double* dir_override,
-                                        const double* cdf = nullptr) {
+                                        const double* cdf = nullptr,
+                                        const uint8_t* guide = nullptr) {
   const LevelDesc& L = P.lv[0];
   int ci, cj, ck;
   decode_cell(P, cell, ci, cj, ck);
@@ -467,6 +468,8 @@ __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
   int n, g;
   if (cdf)
     sample_band_cdf(P, cdf, r_n, r_g, n, g);
+  else if (guide)
+    sample_band_guided(P, guide, r_n, r_g, n, g);
   else
     sample_band(P, r_n, r_g, n, g);
   r.band = n;
@@ -799,6 +802,11 @@ template <int kHint, bool kBrick, bool kPos = true, bool kMulti = false, bool kR
 struct Fp64Lean {
   static_assert(!kMulti || (kPos && !kBrick), "demotion reads positions, k-fastest levels");
   static_assert(!kCW || !kBrick, "cell words use the k-fastest layout");
+  // kDiet: a black-wall cell-word tracer needs no wall record (the band is
+  // row / (n_quad (n_temps - 1))) and stages only the CDF guide tables:
+  // 3 per-axis records + guides keep 7 resident blocks inside the 64 KB
+  // shared-memory carveout, leaving 192 KB of L1 to the gathers.
+  static constexpr bool kDiet = kCW && !kReflect;
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
   uint64_t w_cur;  // kCW: the current cell's word
@@ -849,9 +857,12 @@ struct Fp64Lean {
     extern __shared__ int4 s_dyn[];
     ax = s_dyn + threadIdx.x;
     Ray r;
-    const double* cdf =
-        P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock) : nullptr;
-    const int e = init_ray<true, kCW>(P, cell, ray, r, nullptr, cdf);
+    const double* cdf = !kDiet && P.cdf_smem
+                            ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock)
+                            : nullptr;
+    const uint8_t* guide =
+        kDiet && P.cdf_smem ? reinterpret_cast<const uint8_t*>(s_dyn + 3 * kBlock) : nullptr;
+    const int e = init_ray<true, kCW>(P, cell, ray, r, nullptr, cdf, guide);
     if (e != kErrNone) return e;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -868,8 +879,9 @@ struct Fp64Lean {
     steps_ = 0;
     lvl = 0;
     sal_ = 0;
-    ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
-                               static_cast<int>(cell), static_cast<int>(ray));
+    if (!kDiet)
+      ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
+                                 static_cast<int>(cell), static_cast<int>(ray));
     if (kCW)
       w_cur = __ldg(P.lv[0].cellw + cell);
     else
@@ -1023,7 +1035,8 @@ struct Fp64Lean {
     // stays in its boundary cell (its record still says 0 cells left).
     const bool at_hi = rec.z > 0;
     const int face = 2 * axis + (at_hi ? 1 : 0);
-    const int4 r3 = ax[3 * kBlock];
+    const int4 r3 = kDiet ? make_int4(row / (P.n_quad * (P.n_temps - 1)), 0, 0, 0)
+                          : ax[3 * kBlock];
     const double ew = P.wall_eps[face];
     const double ib_w = __ldg(P.wall_ib + face * P.n_bands + r3.x);
     q += P.qe * tau * ew * div_rcp(ib_w - ib1, ib1, rib1) * pref;
@@ -1134,7 +1147,12 @@ template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = f
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
+  if (P.cdf_smem) {
+    if (kCW && !kPos)  // Fp64Lean::kDiet
+      stage_guides(P, reinterpret_cast<uint8_t*>(s_dyn + 3 * kBlock));
+    else
+      stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
+  }
   pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
 }
 
@@ -1143,7 +1161,12 @@ template <int kMinBlocks, bool kReflect = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
+  if (P.cdf_smem) {
+    if (kCW && !kReflect)  // Fp64Lean::kDiet
+      stage_guides(P, reinterpret_cast<uint8_t*>(s_dyn + 3 * kBlock));
+    else
+      stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
+  }
   pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
 }
 
@@ -1424,6 +1447,10 @@ bool lean_path(const TraceParams& P) {
 }
 size_t fp64_smem(const TraceParams& P) {
   if (!lean_path(P)) return 0;
+  if (P.cellw && !P.track_pos)  // Fp64Lean::kDiet: 3 records + the CDF guides
+    return 3 * kBlock * sizeof(int4) +
+           (P.cdf_smem ? (static_cast<size_t>(kGuideBand) + P.n_bands * kGuideQuad + 15) / 16 * 16
+                       : 0);
   return kLeanRecs64 * kBlock * sizeof(int4) +
          (P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad) : 0);
 }
