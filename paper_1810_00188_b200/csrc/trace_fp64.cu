@@ -806,7 +806,7 @@ struct Fp64Lean {
   // row / (n_quad (n_temps - 1))) and stages only the CDF guide tables:
   // 3 per-axis records + guides keep 7 resident blocks inside the 64 KB
   // shared-memory carveout, leaving 192 KB of L1 to the gathers.
-  static constexpr bool kDiet = kCW && !kReflect;
+  static constexpr bool kDiet = kCW && !kReflect && !kMulti;  // multigrid: measured -0.9 %
   double pos[3], dir[3], tn[3];
   double tau, q, last_ib2, ib1, rib1, pref, t_cur;
   uint64_t w_cur;  // kCW: the current cell's word
@@ -1161,12 +1161,7 @@ template <int kMinBlocks, bool kReflect = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem) {
-    if (kCW && !kReflect)  // Fp64Lean::kDiet
-      stage_guides(P, reinterpret_cast<uint8_t*>(s_dyn + 3 * kBlock));
-    else
-      stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
-  }
+  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
   pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
 }
 
@@ -1447,7 +1442,7 @@ bool lean_path(const TraceParams& P) {
 }
 size_t fp64_smem(const TraceParams& P) {
   if (!lean_path(P)) return 0;
-  if (P.cellw && !P.track_pos)  // Fp64Lean::kDiet: 3 records + the CDF guides
+  if (P.cellw && !P.track_pos && P.n_levels == 1)  // Fp64Lean::kDiet: 3 records + guides
     return 3 * kBlock * sizeof(int4) +
            (P.cdf_smem ? (static_cast<size_t>(kGuideBand) + P.n_bands * kGuideQuad + 15) / 16 * 16
                        : 0);
