@@ -823,8 +823,20 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.t_first = v.temps[0];
   P.t_last = v.temps[v.nt - 1];
   P.steps_per_level = s->d_steps.p;
-  P.cdf_smem = tune().cdf_smem && v.nb * (1 + v.nq) <= ermc_dev::kMaxSmemCdf &&
-                       v.nb <= 255 && v.nq <= 255 ? 1 : 0;
+  // Staged sampling tables (device_common.cuh stage_sampling): the CDFs +
+  // guide tables while they are small (<= 4 KB), else the guides only — a
+  // 119-band CDF (16 KB) in every block took the L1 from the gathers
+  // (fp32, 119 x 16: L1 hit rate 0.4 %). ERMC_CDF_SMEM: 0 off, 1 this
+  // choice, 2 guides only, 3 CDFs + guides whenever they fit 16 KB.
+  {
+    const int mode = tune().cdf_smem;
+    const int len = v.nb * (1 + v.nq);
+    const bool guides = v.nb <= 255 && v.nq <= 255;
+    P.cdf_smem = !guides || mode == 0 ? 0
+                 : mode == 2          ? 2
+                 : mode == 3          ? (len <= ermc_dev::kMaxSmemCdf ? 1 : 2)
+                                      : (len <= 512 ? 1 : 2);
+  }
   P.cdf_guide = s->d_cdf_guide.p;
   // Positions matter after a wall only if some wall can reflect.
   P.track_pos = 0;

@@ -151,10 +151,15 @@ __device__ __forceinline__ int upper_bound_gen(const double* a, int n, double x)
 // quad_cdf[nb][nq], right after the kernel's per-thread records.
 
 // Bytes of the staged CDFs and their guide tables (16-byte multiple).
+__host__ __device__ inline size_t cdf_guide_bytes(int nb) {
+  return (static_cast<size_t>(kGuideBand) + static_cast<size_t>(nb) * kGuideQuad + 15) / 16 * 16;
+}
 __host__ __device__ inline size_t cdf_smem_bytes(int nb, int nq) {
-  const size_t guide = (static_cast<size_t>(kGuideBand) + static_cast<size_t>(nb) * kGuideQuad +
-                        15) / 16 * 16;
-  return static_cast<size_t>(nb) * (1 + nq) * sizeof(double) + guide;
+  return static_cast<size_t>(nb) * (1 + nq) * sizeof(double) + cdf_guide_bytes(nb);
+}
+// Staged bytes for a TraceParams::cdf_smem mode.
+__host__ __device__ inline size_t cdf_stage_bytes(int mode, int nb, int nq) {
+  return mode == 1 ? cdf_smem_bytes(nb, nq) : mode == 2 ? cdf_guide_bytes(nb) : 0;
 }
 
 __device__ __forceinline__ void stage_cdfs(const TraceParams& P, double* dst) {
@@ -199,6 +204,18 @@ __device__ __forceinline__ void sample_band_guided(const TraceParams& P, const u
   if (g >= nq) g = nq - 1;
 }
 
+// Stages per P.cdf_smem at `dst` (after the kernel's per-thread records).
+__device__ __forceinline__ void stage_guides(const TraceParams& P, uint8_t* dst);
+__device__ __forceinline__ void stage_sampling(const TraceParams& P, void* dst) {
+  if (P.cdf_smem == 1) stage_cdfs(P, reinterpret_cast<double*>(dst));
+  else if (P.cdf_smem == 2) stage_guides(P, reinterpret_cast<uint8_t*>(dst));
+}
+// sample_band for the staged mode: `staged` points at what stage_sampling
+// wrote (null: nothing staged).
+__device__ __forceinline__ void sample_band_guided(const TraceParams& P, const uint8_t* guide,
+                                                   double r_n, double r_g, int& n, int& g);
+__device__ __forceinline__ void sample_band_staged(const TraceParams& P, const void* staged,
+                                                   double r_n, double r_g, int& n, int& g);
 __device__ __forceinline__ void stage_guides(const TraceParams& P, uint8_t* dst) {
   for (int i = threadIdx.x; i < kGuideBand + P.n_bands * kGuideQuad; i += blockDim.x)
     dst[i] = P.cdf_guide[i];
@@ -214,6 +231,17 @@ __device__ __forceinline__ void sample_band(const TraceParams& P, double r_n,
                     r_g);
   if (g >= P.n_quad) g = P.n_quad - 1;
 }
+
+__device__ __forceinline__ void sample_band_staged(const TraceParams& P, const void* staged,
+                                                   double r_n, double r_g, int& n, int& g) {
+  if (staged && P.cdf_smem == 1)
+    sample_band_cdf(P, reinterpret_cast<const double*>(staged), r_n, r_g, n, g);
+  else if (staged && P.cdf_smem == 2)
+    sample_band_guided(P, reinterpret_cast<const uint8_t*>(staged), r_n, r_g, n, g);
+  else
+    sample_band(P, r_n, r_g, n, g);
+}
+
 
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   return (__umulhi(n, f.m) + n) >> f.s;

@@ -84,7 +84,9 @@ struct TraceParams {
   const double4* iv64;       // [n_bands*n_quad][n_temps-1] {k_lo, k_hi, ib_lo, ib_hi}
   double inv_dt;             // 1/dt for the table-index estimate
   double inv_w;              // RN(1 / dt): tint's reciprocal when tint_arith
-  int32_t cdf_smem;          // lean kernels stage the sampling CDFs in shared memory
+  int32_t cdf_smem;          // lean kernels stage in shared memory: 0 nothing, 1 the
+                             // sampling CDFs + their guide tables, 2 the guides only
+                             // (large CDFs stay in L1-cached global memory)
   const uint8_t* cdf_guide;  // [kGuideBand + n_bands * kGuideQuad] (with cdf_smem)
   int32_t tint_arith;        // every node is exactly l*dt + t0 and every width
                              // exactly dt, so tint[l] is computed, not loaded

@@ -60,13 +60,13 @@ __device__ __forceinline__ int locate32(const LevelDesc& C, int a, float p, floa
 
 // Sampling CDFs staged after the lean kernels' 3 x kBlock32 per-axis records.
 constexpr int kRecs32 = 3;
-__device__ __forceinline__ const double* staged_cdf(const TraceParams& P) {
+__device__ __forceinline__ const void* staged_cdf(const TraceParams& P) {
   extern __shared__ int4 s_dyn[];
-  return P.cdf_smem ? reinterpret_cast<const double*>(s_dyn + kRecs32 * kBlock32) : nullptr;
+  return P.cdf_smem ? s_dyn + kRecs32 * kBlock32 : nullptr;
 }
 __device__ __forceinline__ void stage_cdfs32(const TraceParams& P) {
   extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kRecs32 * kBlock32));
+  stage_sampling(P, s_dyn + kRecs32 * kBlock32);
 }
 
 struct Fp32Tracer {
@@ -119,7 +119,7 @@ struct Fp32Tracer {
 
   // cdf: sampling CDFs staged in shared memory by the lean kernels, or null.
   __device__ __forceinline__ int init(const TraceParams& P, int64_t cell,
-                                      uint32_t ray, const double* cdf = nullptr) {
+                                      uint32_t ray, const void* cdf = nullptr) {
     const LevelDesc& L = P.lv[0];
     int ci, cj, ck;
     decode_cell(P, cell, ci, cj, ck);
@@ -138,10 +138,7 @@ struct Fp32Tracer {
     dir[1] = sin_t * sp;
     dir[2] = cos_t;
     int n, g;
-    if (cdf)
-      sample_band_cdf(P, cdf, r_n, r_g, n, g);
-    else
-      sample_band(P, r_n, r_g, n, g);
+    sample_band_staged(P, cdf, r_n, r_g, n, g);
     band = n;
     const int nt1 = P.n_temps - 1;
     row = P.iv32 + (static_cast<int64_t>(n) * P.n_quad + g) * nt1;
@@ -892,7 +889,7 @@ bool fp32_lean(const TraceParams& P) { return P.lean != 0; }
 size_t fp32_smem(const TraceParams& P) {
   if (!fp32_lean(P)) return 0;
   return kRecs32 * kBlock32 * sizeof(int4) +
-         (P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad) : 0);
+         cdf_stage_bytes(P.cdf_smem, P.n_bands, P.n_quad);
 }
 TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   // 8 blocks/SM (64 registers) measured best; 10 and 12 lose (0.98, 0.92x).

@@ -437,7 +437,7 @@ template <bool kLean = false, bool kCW = false>
 __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
                                         uint32_t ray_id, Ray& r,
                                         const double* dir_override,
-                                        const double* cdf = nullptr,
+                                        const void* staged = nullptr,
                                         const uint8_t* guide = nullptr) {
   const LevelDesc& L = P.lv[0];
   int ci, cj, ck;
@@ -466,12 +466,10 @@ __device__ __forceinline__ int init_ray(const TraceParams& P, int64_t cell,
   }
 
   int n, g;
-  if (cdf)
-    sample_band_cdf(P, cdf, r_n, r_g, n, g);
-  else if (guide)
+  if (guide)
     sample_band_guided(P, guide, r_n, r_g, n, g);
   else
-    sample_band(P, r_n, r_g, n, g);
+    sample_band_staged(P, staged, r_n, r_g, n, g);
   r.band = n;
   r.quad = g;
   r.krow = P.k + (static_cast<int64_t>(n) * P.n_quad + g) * P.n_temps;
@@ -857,12 +855,10 @@ struct Fp64Lean {
     extern __shared__ int4 s_dyn[];
     ax = s_dyn + threadIdx.x;
     Ray r;
-    const double* cdf = !kDiet && P.cdf_smem
-                            ? reinterpret_cast<const double*>(s_dyn + kLeanRecs64 * kBlock)
-                            : nullptr;
+    const void* staged = !kDiet && P.cdf_smem ? s_dyn + kLeanRecs64 * kBlock : nullptr;
     const uint8_t* guide =
         kDiet && P.cdf_smem ? reinterpret_cast<const uint8_t*>(s_dyn + 3 * kBlock) : nullptr;
-    const int e = init_ray<true, kCW>(P, cell, ray, r, nullptr, cdf, guide);
+    const int e = init_ray<true, kCW>(P, cell, ray, r, nullptr, staged, guide);
     if (e != kErrNone) return e;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -1151,7 +1147,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     if (kCW && !kPos)  // Fp64Lean::kDiet
       stage_guides(P, reinterpret_cast<uint8_t*>(s_dyn + 3 * kBlock));
     else
-      stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
+      stage_sampling(P, s_dyn + kLeanRecs64 * kBlock);
   }
   pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
 }
@@ -1161,7 +1157,7 @@ template <int kMinBlocks, bool kReflect = true, bool kCW = false>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
-  if (P.cdf_smem) stage_cdfs(P, reinterpret_cast<double*>(s_dyn + kLeanRecs64 * kBlock));
+  stage_sampling(P, s_dyn + kLeanRecs64 * kBlock);
   pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
 }
 
@@ -1443,11 +1439,8 @@ bool lean_path(const TraceParams& P) {
 size_t fp64_smem(const TraceParams& P) {
   if (!lean_path(P)) return 0;
   if (P.cellw && !P.track_pos && P.n_levels == 1)  // Fp64Lean::kDiet: 3 records + guides
-    return 3 * kBlock * sizeof(int4) +
-           (P.cdf_smem ? (static_cast<size_t>(kGuideBand) + P.n_bands * kGuideQuad + 15) / 16 * 16
-                       : 0);
-  return kLeanRecs64 * kBlock * sizeof(int4) +
-         (P.cdf_smem ? cdf_smem_bytes(P.n_bands, P.n_quad) : 0);
+    return 3 * kBlock * sizeof(int4) + (P.cdf_smem ? cdf_guide_bytes(P.n_bands) : 0);
+  return kLeanRecs64 * kBlock * sizeof(int4) + cdf_stage_bytes(P.cdf_smem, P.n_bands, P.n_quad);
 }
 // min_blocks = 0 picks the measured best per variant (B200, 256^3 channel):
 // 8 blocks/SM for the black-wall tracer (64 registers + 128 B of L1-resident
