@@ -119,3 +119,38 @@ def test_config4_fp32_within_3sigma_of_reference(channel256):
             rel = np.abs(q[cells] - rq) / np.maximum(np.abs(rq), 1e-6 * np.abs(rq).max())
             assert np.median(rel) < 1e-3, np.median(rel)
             assert bad == 0
+
+
+@pytest.mark.parametrize("variant", [
+    dict(wall_eps=0.5),                                   # grey walls: diffuse reflection tracer
+    dict(wall_eps=0.5, specular_walls=1),                 # specular reflection
+    dict(n_levels=7, steps_per_level=5, coarsen_ratio=2),  # 7-level multigrid, black walls
+    dict(precision_fp32=True, n_levels=7, steps_per_level=5, coarsen_ratio=2),
+])
+def test_headline_field_variants_match_reference(variant):
+    # The config-4 field with the tracers the bench line does not time: grey
+    # walls (position tracking, reflection) and multigrid ray coarsening,
+    # R = 16, checked like the headline (fp32: 3 sigma, the same rays).
+    v = dict(variant)
+    eps = v.pop("wall_eps", 1.0)
+    fp32 = v.pop("precision_fp32", False)
+    grid, t, b, m, _ = W.channel_case(N, "nongrey16", wall_eps=eps)
+    runs = W.stratified_runs(N, 64, 16)
+    if not fp32:
+        cfg = capi.config_struct(rays_per_cell=16, seed=11, **v)
+        sess, td, q, sd, st = _whole_field(grid, t, b, m, cfg)
+        try:
+            rep = headline.check(grid, t, b, m, cfg, q, sd, headline.torch_range_solver(sess),
+                                 runs)
+        finally:
+            sess.close()
+        print(variant, rep)
+        assert rep["ok"], rep
+        return
+    cfg32 = capi.config_struct(rays_per_cell=16, seed=11, precision=capi.FP32, **v)
+    sess, td, q, sd, st = _whole_field(grid, t, b, m, cfg32)
+    sess.close()
+    cells = headline.sample_cells(runs)
+    rq, rsd, _, _ = refshim.solve_cells(grid, t, b, m,
+                                        capi.config_struct(rays_per_cell=16, seed=11, **v), cells)
+    assert three_sigma_violations(q[cells], rq, sd[cells], rsd) == 0
