@@ -626,10 +626,18 @@ def spawn_ranks(a):
                    LOCAL_WORLD_SIZE=str(a.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         procs.append(subprocess.Popen([sys.executable, *sys.argv], env=env,
                                       stdout=None if r == 0 else subprocess.DEVNULL))
-    rc = 0
-    for pr in procs:
-        rc = max(rc, pr.wait())
-    return rc
+    # A rank that fails would leave the others blocked in a collective: stop
+    # them (these are our own children, by PID) and report the failure.
+    while True:
+        codes = [pr.poll() for pr in procs]
+        if any(c not in (None, 0) for c in codes):
+            for pr in procs:
+                if pr.poll() is None:
+                    pr.kill()
+            return max(c for c in (pr.wait() for pr in procs) if c is not None) or 1
+        if all(c == 0 for c in codes):
+            return 0
+        time.sleep(0.5)
 
 
 def main():
