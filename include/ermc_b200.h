@@ -242,6 +242,57 @@ int ermc_b200_trace_rays(const ermc_grid_t* grid, const double* temperature,
                          const double* dir_override, ermc_ray_result_t* out,
                          int64_t* level_steps, char* errbuf, size_t errlen);
 
+/* ---- The per-ray API of the reference (sampling.hpp, tracer.hpp), on the
+ * GPU. Each call runs the device code of the trace kernels on n explicit
+ * rays; the C++ API (ermc_b200.hpp: sample_direction, init_ray, march,
+ * absorptivity) wraps them one ray at a time. ---- */
+
+/* RayState (reference sampling.hpp:36-51): cell = {i, j, k, level}. */
+typedef struct ermc_ray_state {
+  double pos[3];
+  double dir[3];
+  int32_t cell[4];
+  double transmissivity;
+  int32_t band, quad;
+  double prefactor;   /* R_I */
+  double ib_source;
+  int32_t reflections;
+  int32_t reserved0;
+  uint64_t seed;
+  uint64_t cell_id;
+  uint32_t ray_id;
+  uint32_t next_draw;
+} ermc_ray_state_t;
+
+/* sample_direction (reference sampling.cpp:31-40) for n draw pairs:
+ * out[5 i + 0..4] = theta, phi, unit[0..2]. */
+int ermc_b200_sample_direction(int64_t n, const double* r_theta, const double* r_phi,
+                               double* out, char* errbuf, size_t errlen);
+/* absorptivity (reference tracer.cpp:11-13): out[i] = -expm1(-kappa[i] ds[i]). */
+int ermc_b200_absorptivity(int64_t n, const double* kappa, const double* ds, double* out,
+                           char* errbuf, size_t errlen);
+/* init_ray (reference sampling.cpp:55-96) for n (cell, ray) pairs on the
+ * level-0 grid / field, with the given sampling CDFs (band_cdf[n_bands],
+ * quad_cdf[n_bands * n_quad]) built at t_max. cells = 3 n (i, j, k). */
+int ermc_b200_init_rays(const ermc_grid_t* grid, const double* temperature,
+                        const ermc_model_t* model, const double* band_cdf,
+                        const double* quad_cdf, double t_max, uint64_t seed,
+                        int32_t volume_sampling, int64_t n, const int32_t* cells,
+                        const uint32_t* ray_ids, ermc_ray_state_t* out, char* errbuf,
+                        size_t errlen);
+/* march (reference tracer.cpp:57-194) of n ray states through a grid
+ * hierarchy given level by level (grids[l], fields[l] k-fastest,
+ * step_caps[l], -1 = uncapped), with TraceOptions {tolerance, max_steps,
+ * specular}. out: q_contribution, weights, steps, termination, reflections;
+ * level_steps[n * n_levels] when non-NULL. */
+int ermc_b200_march_rays(int32_t n_levels, const ermc_grid_t* grids,
+                         const double* const* fields, const int32_t* step_caps,
+                         const ermc_model_t* model, const ermc_boundary_t* boundary,
+                         double q_emission, double tolerance, int64_t max_steps,
+                         int32_t specular, int64_t n, const ermc_ray_state_t* rays,
+                         ermc_ray_result_t* out, int64_t* level_steps, char* errbuf,
+                         size_t errlen);
+
 /* ---- Host setup the kernel consumes (bitwise the reference's). ---- */
 
 /* build_cdfs (reference spectral.cpp:306-354): band_cdf[n_bands],

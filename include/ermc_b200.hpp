@@ -19,6 +19,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ermc_b200.h"
@@ -259,6 +260,71 @@ struct SolutionField {
   std::int64_t total_steps = 0;
   double wall_time = 0.0;
 };
+
+// ---- sampling.hpp / tracer.hpp: the per-ray API --------------------------
+// The reference's per-ray functions (sampling.hpp:13-58, tracer.hpp:12-42).
+// init_ray, march, sample_direction and absorptivity run the trace kernels'
+// device code on the GPU, one ray per call (ermc_b200_init_rays,
+// _march_rays, _sample_direction, _absorptivity); uniform and sample_band
+// are the integer hash and CDF search the GPU solve and presample_and_sort
+// share (pure functions, bitwise the device's).
+struct RandomKey {
+  std::uint64_t seed = 0;
+  std::uint64_t cell_id = 0;
+  std::uint32_t ray_id = 0;
+  std::uint32_t draw_id = 0;
+};
+double uniform(const RandomKey& key);
+
+struct Direction {
+  double theta = 0.0;
+  double phi = 0.0;
+  Vec3 unit = {0.0, 0.0, 1.0};
+};
+Direction sample_direction(double r_theta, double r_phi);
+std::pair<int, int> sample_band(double r_n, double r_g, const SamplingCdfs& cdfs);
+
+struct RayState {
+  Vec3 pos = {0.0, 0.0, 0.0};
+  Vec3 dir = {0.0, 0.0, 1.0};
+  CellIndex cell;
+  double transmissivity = 1.0;
+  int band = 0;
+  int quad = 0;
+  double prefactor = 1.0;
+  double ib_source = 0.0;
+  int reflections = 0;
+  std::uint64_t seed = 0;
+  std::uint64_t cell_id = 0;
+  std::uint32_t ray_id = 0;
+  std::uint32_t next_draw = 0;
+};
+RayState init_ray(const CellIndex& cell, std::uint32_t ray_id, std::uint64_t seed,
+                  const SpectralModel& model, const SamplingCdfs& cdfs,
+                  const GridHierarchy& hierarchy, bool volume_sampling = false);
+
+enum class Termination { tolerance, wall_absorbed, step_cap };
+
+struct MarchResult {
+  double q_contribution = 0.0;
+  std::int64_t steps = 0;
+  std::vector<std::int64_t> steps_per_level;
+  Termination terminated_by = Termination::tolerance;
+  int reflections = 0;
+  double weight_absorbed = 0.0;
+  double weight_walls = 0.0;
+  double weight_residual = 0.0;
+};
+
+struct TraceOptions {
+  double tolerance = 1e-4;
+  std::int64_t max_steps = 100000;
+  bool specular_walls = false;
+};
+
+MarchResult march(RayState ray, const GridHierarchy& hierarchy, const SpectralModel& model,
+                  const BoundarySpec& boundary, double q_emission, const TraceOptions& options);
+double absorptivity(double kappa, double ds);
 
 // presample_and_sort (reference solver.hpp:39-50, solver.cpp:62-80): the
 // (band, g) of every ray of a cell from its keyed draws 2 and 3, ordered by

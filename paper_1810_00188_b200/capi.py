@@ -69,6 +69,14 @@ class RayResult(C.Structure):
                 ("reserved0", C.c_int32)]
 
 
+class RayState(C.Structure):
+    _fields_ = [("pos", C.c_double * 3), ("dir", C.c_double * 3), ("cell", C.c_int32 * 4),
+                ("transmissivity", C.c_double), ("band", C.c_int32), ("quad", C.c_int32),
+                ("prefactor", C.c_double), ("ib_source", C.c_double),
+                ("reflections", C.c_int32), ("reserved0", C.c_int32), ("seed", C.c_uint64),
+                ("cell_id", C.c_uint64), ("ray_id", C.c_uint32), ("next_draw", C.c_uint32)]
+
+
 EXPORTS = {
     "ermc_b200_config_default": (None, [C.POINTER(Config)]),
     "ermc_b200_solve": (C.c_int, [C.POINTER(Grid), _d, C.POINTER(Boundary),
@@ -109,6 +117,18 @@ EXPORTS = {
                                        C.c_double, C.c_int64, C.POINTER(C.c_int64),
                                        C.POINTER(C.c_uint32), _d, C.POINTER(RayResult),
                                        C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
+    "ermc_b200_sample_direction": (C.c_int, [C.c_int64, _d, _d, _d, C.c_char_p, C.c_size_t]),
+    "ermc_b200_absorptivity": (C.c_int, [C.c_int64, _d, _d, _d, C.c_char_p, C.c_size_t]),
+    "ermc_b200_init_rays": (C.c_int, [C.POINTER(Grid), _d, C.POINTER(Model), _d, _d, C.c_double,
+                                      C.c_uint64, C.c_int32, C.c_int64, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_uint32), C.POINTER(RayState), C.c_char_p,
+                                      C.c_size_t]),
+    "ermc_b200_march_rays": (C.c_int, [C.c_int32, C.POINTER(Grid), C.POINTER(_d),
+                                       C.POINTER(C.c_int32), C.POINTER(Model),
+                                       C.POINTER(Boundary), C.c_double, C.c_double, C.c_int64,
+                                       C.c_int32, C.c_int64, C.POINTER(RayState),
+                                       C.POINTER(RayResult), C.POINTER(C.c_int64), C.c_char_p,
+                                       C.c_size_t]),
     "ermc_b200_build_cdfs": (C.c_int, [C.POINTER(Model), C.c_double, _d, _d,
                                        C.c_char_p, C.c_size_t]),
     "ermc_b200_planck_mean": (C.c_int, [C.POINTER(Model), C.c_double, _d, C.c_char_p,

@@ -65,6 +65,16 @@ cudaError_t launch_to_bricked64(const double* src, double* dst, int nx, int ny, 
                                 cudaStream_t s);
 cudaError_t launch_build_cell_words(const TraceParams& P, const double* field, int64_t n,
                                     double scale, uint64_t* out, int* bad, cudaStream_t s);
+cudaError_t launch_init_states_fp64(const TraceParams& P, int64_t n, const int32_t* cells,
+                                    const uint32_t* ray_ids, uint64_t seed,
+                                    ermc_ray_state_t* out, int32_t* err, cudaStream_t s);
+cudaError_t launch_march_states_fp64(const TraceParams& P, int64_t n,
+                                     const ermc_ray_state_t* in, RayRecord* out,
+                                     int64_t* level_steps, cudaStream_t s);
+cudaError_t launch_sample_direction(int64_t n, const double* rt, const double* rp, double* out,
+                                    cudaStream_t s);
+cudaError_t launch_absorptivity(int64_t n, const double* k, const double* ds, double* out,
+                                cudaStream_t s);
 int sort_max_bins();
 int sort_max_tile_items();
 cudaError_t launch_ng_sort(const TraceParams& P, const int32_t* row_rank, int n_rows,
@@ -1618,6 +1628,189 @@ int ermc_b200_trace_rays(const ermc_grid_t* grid, const double* temperature,
       o.band = r.band;
       o.quad = r.quad;
       o.next_draw = r.next_draw;
+    }
+  });
+}
+
+namespace {
+void require_device() {
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+    cudaGetLastError();
+    throw Error("ermc_b200: no CUDA device available (the solver has no CPU path)");
+  }
+}
+
+// The reference's RayRecord -> ermc_ray_result_t (ermc_b200_trace_rays too).
+void copy_result(const ermc_dev::RayRecord& r, ermc_ray_result_t& o) {
+  std::memset(&o, 0, sizeof(o));
+  o.q_contribution = r.q;
+  o.weight_absorbed = r.w_abs;
+  o.weight_walls = r.w_walls;
+  o.weight_residual = r.w_res;
+  for (int a = 0; a < 3; ++a) o.dir[a] = r.dir[a];
+  o.prefactor = r.prefactor;
+  o.ib_source = r.ib_source;
+  o.steps = r.steps;
+  o.terminated_by = r.term;
+  o.reflections = r.reflections;
+  o.band = r.band;
+  o.quad = r.quad;
+  o.next_draw = r.next_draw;
+}
+}  // namespace
+
+int ermc_b200_sample_direction(int64_t n, const double* r_theta, const double* r_phi,
+                               double* out, char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    require_device();
+    if (n <= 0) return;
+    cudaStream_t st = nullptr;
+    DevBuf<double> a, b, o;
+    a.upload(r_theta, n, st);
+    b.upload(r_phi, n, st);
+    o.ensure(5 * static_cast<size_t>(n));
+    cuda_check(ermc_dev::launch_sample_direction(n, a.p, b.p, o.p, st), "sample_direction");
+    cuda_check(cudaMemcpy(out, o.p, 5 * n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int ermc_b200_absorptivity(int64_t n, const double* kappa, const double* ds, double* out,
+                           char* errbuf, size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    require_device();
+    if (n <= 0) return;
+    cudaStream_t st = nullptr;
+    DevBuf<double> a, b, o;
+    a.upload(kappa, n, st);
+    b.upload(ds, n, st);
+    o.ensure(n);
+    cuda_check(ermc_dev::launch_absorptivity(n, a.p, b.p, o.p, st), "absorptivity");
+    cuda_check(cudaMemcpy(out, o.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int ermc_b200_init_rays(const ermc_grid_t* grid, const double* temperature,
+                        const ermc_model_t* model, const double* band_cdf,
+                        const double* quad_cdf, double t_max, uint64_t seed,
+                        int32_t volume_sampling, int64_t n, const int32_t* cells,
+                        const uint32_t* ray_ids, ermc_ray_state_t* out, char* errbuf,
+                        size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    ermc_config_t cfg;
+    ermc_b200_config_default(&cfg);
+    cfg.rays_per_cell = 1;
+    cfg.seed = seed;
+    cfg.volume_sampling = volume_sampling;
+    ermc_boundary_t b{};  // init_ray reads no wall
+    for (int a = 0; a < 3; ++a) {
+      b.kind[a] = ERMC_AXIS_PERIODIC;
+      b.lo_emissivity[a] = b.hi_emissivity[a] = 1.0;
+    }
+    std::unique_ptr<ermc_session> s(create_session(grid, &b, model, &cfg));
+    DeviceGuard guard(s->device);
+    cudaStream_t st = nullptr;
+    set_field_impl(s.get(), temperature, 0, st);
+    Prepared pr;
+    prepare(s.get(), pr, t_max, 1.0, false, st);
+    // the caller's CDFs (a SamplingCdfs need not come from build_cdfs)
+    const ermc_host::TableView& v = s->view;
+    s->d_band_cdf.upload(band_cdf, v.nb, st);
+    s->d_quad_cdf.upload(quad_cdf, static_cast<size_t>(v.nb) * v.nq, st);
+    pr.P.band_cdf = s->d_band_cdf.p;
+    pr.P.quad_cdf = s->d_quad_cdf.p;
+    DevBuf<int32_t> dc, de;
+    DevBuf<uint32_t> dr;
+    DevBuf<ermc_ray_state_t> dout;
+    dc.upload(cells, 3 * static_cast<size_t>(n), st);
+    dr.upload(ray_ids, n, st);
+    de.ensure(n);
+    dout.ensure(n);
+    cuda_check(ermc_dev::launch_init_states_fp64(pr.P, n, dc.p, dr.p, seed, dout.p, de.p, st),
+               "init_rays");
+    std::vector<int32_t> errs(n);
+    cuda_check(cudaMemcpy(errs.data(), de.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost),
+               "D2H");
+    for (int64_t i = 0; i < n; ++i)
+      if (errs[i] != ermc_dev::kErrNone) {
+        ermc_dev::RayRecord rec{};
+        rec.err = errs[i];
+        rec.err_value = temperature[(static_cast<int64_t>(cells[3 * i]) * grid->ny +
+                                     cells[3 * i + 1]) * grid->nz + cells[3 * i + 2]];
+        throw Error(error_message(s.get(), rec, 0, ray_ids[i]));
+      }
+    cuda_check(cudaMemcpy(out, dout.p, n * sizeof(ermc_ray_state_t), cudaMemcpyDeviceToHost),
+               "D2H");
+  });
+}
+
+int ermc_b200_march_rays(int32_t n_levels, const ermc_grid_t* grids,
+                         const double* const* fields, const int32_t* step_caps,
+                         const ermc_model_t* model, const ermc_boundary_t* boundary,
+                         double q_emission, double tolerance, int64_t max_steps,
+                         int32_t specular, int64_t n, const ermc_ray_state_t* rays,
+                         ermc_ray_result_t* out, int64_t* level_steps, char* errbuf,
+                         size_t errlen) {
+  return guarded(errbuf, errlen, [&] {
+    if (n_levels < 1 || n_levels > ermc_dev::kMaxLevels)
+      throw Error("march: hierarchy must have 1 to 16 levels");
+    ermc_config_t cfg;
+    ermc_b200_config_default(&cfg);
+    cfg.rays_per_cell = 1;
+    std::unique_ptr<ermc_session> s(create_session(&grids[0], boundary, model, &cfg));
+    DeviceGuard guard(s->device);
+    cudaStream_t st = nullptr;
+    set_field_impl(s.get(), fields[0], 0, st);
+    Prepared pr;
+    prepare(s.get(), pr, s->temps.back(), q_emission, false, st);  // T_max: CDFs unused
+    ermc_dev::TraceParams& P = pr.P;
+    // the caller's hierarchy, level by level (GridHierarchy, geometry.hpp:74-83)
+    std::vector<DevBuf<double>> lv(n_levels);
+    P.n_levels = n_levels;
+    for (int l = 0; l < n_levels; ++l) {
+      const ermc_grid_t& g = grids[l];
+      validate_grid(g);
+      ermc_dev::LevelDesc& L = P.lv[l];
+      for (int a = 0; a < 3; ++a) {
+        L.n[a] = count(g, a);
+        L.d[a] = spacing(g, a);
+        L.rd[a] = 1.0 / L.d[a];
+        L.origin[a] = g.origin[a];
+        L.extent[a] = count(g, a) * spacing(g, a);
+      }
+      L.eps = 1e-12 * std::min({g.dx, g.dy, g.dz});
+      L.cap = step_caps[l];
+      if (l == 0) {
+        L.field = s->d_field.p;
+      } else {
+        lv[l].upload(fields[l], static_cast<size_t>(cells_of(g)), st);
+        L.field = lv[l].p;
+      }
+    }
+    P.qe = q_emission;
+    P.tol = tolerance;
+    P.max_steps = max_steps;
+    P.specular = specular;
+    DevBuf<ermc_ray_state_t> din;
+    DevBuf<ermc_dev::RayRecord> drec;
+    DevBuf<int64_t> dls;
+    din.upload(rays, n, st);
+    drec.ensure(n);
+    if (level_steps) dls.ensure(static_cast<size_t>(n) * n_levels);
+    cuda_check(ermc_dev::launch_march_states_fp64(P, n, din.p, drec.p,
+                                                  level_steps ? dls.p : nullptr, st),
+               "march_rays");
+    std::vector<ermc_dev::RayRecord> recs(n);
+    cuda_check(cudaMemcpy(recs.data(), drec.p, n * sizeof(ermc_dev::RayRecord),
+                          cudaMemcpyDeviceToHost), "D2H");
+    if (level_steps)
+      cuda_check(cudaMemcpy(level_steps, dls.p, n * n_levels * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t i = 0; i < n; ++i) {
+      if (recs[i].err != ermc_dev::kErrNone)
+        throw Error(error_message(s.get(), recs[i], static_cast<int64_t>(rays[i].cell_id),
+                                  rays[i].ray_id));
+      copy_result(recs[i], out[i]);
     }
   });
 }

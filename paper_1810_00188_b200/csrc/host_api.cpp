@@ -595,6 +595,134 @@ int cdf_index(const std::vector<double>& cdf, double u) {
 }
 }  // namespace
 
+// ---- the per-ray API (reference sampling.cpp, tracer.cpp) -----------------
+double uniform(const RandomKey& key) {
+  return keyed_uniform(key.seed, key.cell_id, key.ray_id, key.draw_id);
+}
+
+std::pair<int, int> sample_band(double r_n, double r_g, const SamplingCdfs& cdfs) {
+  const int n = cdf_index(cdfs.band_cdf, r_n);
+  return {n, cdf_index(cdfs.quad_cdf[n], r_g)};
+}
+
+namespace {
+void check_rc(int rc, const char* err) {
+  if (rc != 0) throw Error(err);
+}
+}  // namespace
+
+Direction sample_direction(double r_theta, double r_phi) {
+  double out[5];
+  char err[512] = {0};
+  check_rc(ermc_b200_sample_direction(1, &r_theta, &r_phi, out, err, sizeof err), err);
+  Direction d;
+  d.theta = out[0];
+  d.phi = out[1];
+  d.unit = {out[2], out[3], out[4]};
+  return d;
+}
+
+double absorptivity(double kappa, double ds) {
+  double out = 0.0;
+  char err[512] = {0};
+  check_rc(ermc_b200_absorptivity(1, &kappa, &ds, &out, err, sizeof err), err);
+  return out;
+}
+
+RayState init_ray(const CellIndex& cell, std::uint32_t ray_id, std::uint64_t seed,
+                  const SpectralModel& model, const SamplingCdfs& cdfs,
+                  const GridHierarchy& hierarchy, bool volume_sampling) {
+  if (hierarchy.grids.empty()) throw Error("init_ray: empty grid hierarchy");
+  const int nb = model.n_bands(), nq = model.n_quad();
+  if (static_cast<int>(cdfs.band_cdf.size()) != nb ||
+      static_cast<int>(cdfs.quad_cdf.size()) != nb)
+    throw Error("init_ray: sampling CDFs do not match the spectral model");
+  std::vector<double> quad(static_cast<size_t>(nb) * nq);
+  for (int n = 0; n < nb; ++n) {
+    if (static_cast<int>(cdfs.quad_cdf[n].size()) != nq)
+      throw Error("init_ray: sampling CDFs do not match the spectral model");
+    std::copy(cdfs.quad_cdf[n].begin(), cdfs.quad_cdf[n].end(), quad.begin() + n * nq);
+  }
+  const ermc_grid_t g = grid_view(hierarchy.grids[0]);
+  const ermc_model_t m = model.c_view();
+  const int32_t c[3] = {cell.i, cell.j, cell.k};
+  ermc_ray_state_t st{};
+  char err[1024] = {0};
+  check_rc(ermc_b200_init_rays(&g, hierarchy.fields[0].data(), &m, cdfs.band_cdf.data(),
+                               quad.data(), cdfs.t_max, seed, volume_sampling ? 1 : 0, 1, c,
+                               &ray_id, &st, err, sizeof err),
+           err);
+  RayState r;
+  r.pos = {st.pos[0], st.pos[1], st.pos[2]};
+  r.dir = {st.dir[0], st.dir[1], st.dir[2]};
+  r.cell = CellIndex{st.cell[0], st.cell[1], st.cell[2], st.cell[3]};
+  r.transmissivity = st.transmissivity;
+  r.band = st.band;
+  r.quad = st.quad;
+  r.prefactor = st.prefactor;
+  r.ib_source = st.ib_source;
+  r.reflections = st.reflections;
+  r.seed = st.seed;
+  r.cell_id = st.cell_id;
+  r.ray_id = st.ray_id;
+  r.next_draw = st.next_draw;
+  return r;
+}
+
+MarchResult march(RayState ray, const GridHierarchy& hierarchy, const SpectralModel& model,
+                  const BoundarySpec& boundary, double q_emission, const TraceOptions& options) {
+  const int nl = hierarchy.n_levels();
+  if (nl < 1 || static_cast<int>(hierarchy.fields.size()) != nl)
+    throw Error("march: invalid grid hierarchy");
+  std::vector<ermc_grid_t> grids(nl);
+  std::vector<const double*> fields(nl);
+  std::vector<int32_t> caps(nl);
+  for (int l = 0; l < nl; ++l) {
+    grids[l] = grid_view(hierarchy.grids[l]);
+    fields[l] = hierarchy.fields[l].data();
+    caps[l] = l < static_cast<int>(hierarchy.step_caps.size()) ? hierarchy.step_caps[l] : -1;
+  }
+  ermc_ray_state_t st{};
+  for (int a = 0; a < 3; ++a) {
+    st.pos[a] = ray.pos[a];
+    st.dir[a] = ray.dir[a];
+  }
+  st.cell[0] = ray.cell.i;
+  st.cell[1] = ray.cell.j;
+  st.cell[2] = ray.cell.k;
+  st.cell[3] = ray.cell.level;
+  st.transmissivity = ray.transmissivity;
+  st.band = ray.band;
+  st.quad = ray.quad;
+  st.prefactor = ray.prefactor;
+  st.ib_source = ray.ib_source;
+  st.reflections = ray.reflections;
+  st.seed = ray.seed;
+  st.cell_id = ray.cell_id;
+  st.ray_id = ray.ray_id;
+  st.next_draw = ray.next_draw;
+  const ermc_model_t m = model.c_view();
+  const ermc_boundary_t b = boundary_view(boundary);
+  ermc_ray_result_t res{};
+  std::vector<std::int64_t> level_steps(nl, 0);
+  char err[1024] = {0};
+  check_rc(ermc_b200_march_rays(nl, grids.data(), fields.data(), caps.data(), &m, &b,
+                                q_emission, options.tolerance, options.max_steps,
+                                options.specular_walls ? 1 : 0, 1, &st, &res,
+                                level_steps.data(), err, sizeof err),
+           err);
+  MarchResult out;
+  out.q_contribution = res.q_contribution;
+  out.steps = res.steps;
+  out.steps_per_level = level_steps;
+  out.terminated_by = static_cast<Termination>(res.terminated_by);
+  out.reflections = res.reflections;
+  out.weight_absorbed = res.weight_absorbed;
+  out.weight_walls = res.weight_walls;
+  out.weight_residual = res.weight_residual;
+  return out;
+}
+
 std::vector<PlanEntry> presample_and_sort(std::uint64_t cell_id, std::uint32_t n_rays,
                                           std::uint64_t seed, const SamplingCdfs& cdfs,
                                           const SpectralModel& model) {

@@ -9,6 +9,8 @@
 
 #include <cstdint>
 
+#include "ermc_b200.h"  // ermc_ray_state_t (the per-ray API's state)
+
 namespace ermc_dev {
 
 constexpr int kMaxLevels = 16;

@@ -1276,6 +1276,133 @@ __global__ void trace_rays_fp64(const __grid_constant__ TraceParams P,
       level_steps[s * P.n_levels + l] = dbg.level_steps[l];
 }
 
+// Per-ray API (ermc_b200_init_rays / _march_rays / _sample_direction /
+// _absorptivity): the reference's init_ray, march, sample_direction and
+// absorptivity (sampling.cpp:31-96, tracer.cpp:11-194) on explicit rays,
+// with the debug tracer's reference-order arithmetic.
+__global__ void init_states_fp64(const __grid_constant__ TraceParams P, int64_t n,
+                                 const int32_t* __restrict__ cells,
+                                 const uint32_t* __restrict__ ray_ids, uint64_t seed,
+                                 ermc_ray_state_t* __restrict__ out, int32_t* __restrict__ err) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= n) return;
+  const LevelDesc& L = P.lv[0];
+  const int64_t cell =
+      (static_cast<int64_t>(cells[3 * s]) * L.n[1] + cells[3 * s + 1]) * L.n[2] + cells[3 * s + 2];
+  Ray r;
+  const int e = init_ray(P, cell, ray_ids[s], r, nullptr);
+  err[s] = e;
+  if (e != kErrNone) return;
+  ermc_ray_state_t o;
+  for (int a = 0; a < 3; ++a) {
+    o.pos[a] = r.pos[a];
+    o.dir[a] = r.dir[a];
+    o.cell[a] = r.idx[a];
+  }
+  o.cell[3] = 0;
+  o.transmissivity = 1.0;
+  o.band = r.band;
+  o.quad = r.quad;
+  o.prefactor = r.pref;
+  o.ib_source = r.ib1;
+  o.reflections = 0;
+  o.reserved0 = 0;
+  o.seed = seed;
+  o.cell_id = static_cast<uint64_t>(cell);
+  o.ray_id = ray_ids[s];
+  o.next_draw = r.next_draw;
+  out[s] = o;
+}
+
+__global__ void march_states_fp64(const __grid_constant__ TraceParams P, int64_t n,
+                                  const ermc_ray_state_t* __restrict__ in,
+                                  RayRecord* __restrict__ out, int64_t* level_steps) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= n) return;
+  const ermc_ray_state_t st = in[s];
+  Ray r;
+  for (int a = 0; a < 3; ++a) {
+    r.pos[a] = st.pos[a];
+    r.dir[a] = st.dir[a];
+    r.idx[a] = st.cell[a];
+  }
+  r.level = st.cell[3];
+  r.tau = st.transmissivity;
+  r.q = 0.0;
+  r.ib1 = st.ib_source;
+  r.last_ib2 = st.ib_source;  // degenerate termination dumps zero (tracer.cpp:67)
+  r.pref = st.prefactor;
+  r.band = st.band;
+  r.quad = st.quad;
+  r.krow = P.k + (static_cast<int64_t>(st.band) * P.n_quad + st.quad) * P.n_temps;
+  r.ibrow = P.ib + static_cast<int64_t>(st.band) * P.n_temps;
+  r.sal = 0;
+  r.steps = 0;
+  r.h_cell = mix64(mix64(st.seed + 0x9e3779b97f4a7c15ULL) ^ st.cell_id);
+  r.ray_id = st.ray_id;
+  r.next_draw = st.next_draw;
+  dda_setup(P.lv[r.level], r);
+  DebugRec dbg;
+  dbg.w_abs = dbg.w_walls = 0.0;
+  dbg.reflections = 0;
+  dbg.term = 0;
+  dbg.err_value = 0.0;
+  dbg.err_axis = -1;
+  for (int l = 0; l < kMaxLevels; ++l) dbg.level_steps[l] = 0;
+  const int max_steps = static_cast<int>(
+      P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL);
+  int stt, e = 0;
+  const bool multi = P.n_levels > 1;
+  do {
+    stt = multi ? march_step<true, true>(P, r, max_steps, &dbg, &e)
+                : march_step<false, true>(P, r, max_steps, &dbg, &e);
+  } while (stt == kContinue);
+  RayRecord rec;
+  rec.err = stt == kFail ? e : kErrNone;
+  rec.err_value = dbg.err_value;
+  rec.err_axis = dbg.err_axis;
+  rec.q = stt == kFail ? r.q : finish_ray(P, r);
+  rec.w_abs = dbg.w_abs;
+  rec.w_walls = dbg.w_walls;
+  rec.w_res = r.tau;
+  for (int a = 0; a < 3; ++a) rec.dir[a] = r.dir[a];
+  rec.prefactor = r.pref;
+  rec.ib_source = r.ib1;
+  rec.steps = r.steps;
+  rec.term = dbg.term;
+  rec.reflections = dbg.reflections;
+  rec.band = r.band;
+  rec.quad = r.quad;
+  rec.next_draw = r.next_draw;
+  out[s] = rec;
+  if (level_steps)
+    for (int l = 0; l < P.n_levels; ++l) level_steps[s * P.n_levels + l] = dbg.level_steps[l];
+}
+
+__global__ void sample_direction_kernel(int64_t n, const double* __restrict__ rt,
+                                        const double* __restrict__ rp, double* __restrict__ out) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= n) return;
+  // sampling.cpp:31-40, the operations of init_ray above
+  const double cos_t = 1.0 - 2.0 * rt[s];
+  const double phi = 2.0 * kPiD * rp[s];
+  const double sin_t = sqrt(fmax(0.0, 1.0 - cos_t * cos_t));
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  out[5 * s + 0] = acos(cos_t);
+  out[5 * s + 1] = phi;
+  out[5 * s + 2] = sin_t * cp;
+  out[5 * s + 3] = sin_t * sp;
+  out[5 * s + 4] = cos_t;
+}
+
+__global__ void absorptivity_kernel(int64_t n, const double* __restrict__ k,
+                                    const double* __restrict__ ds, double* __restrict__ out) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= n) return;
+  out[s] = -expm1(-k[s] * ds[s]);  // the march's alpha (tracer.cpp:118)
+}
+
 // K2: per-cell tally in ray-id order (reference solver.cpp:142-155).
 __device__ __forceinline__ void tally_cell(const double* __restrict__ q_ray, int64_t n_cells,
                                            int rays, int64_t c, double& sum, double& sd) {
@@ -1528,6 +1655,39 @@ cudaError_t launch_trace_rays_fp64(const TraceParams& P, int64_t n,
   const int64_t grid = (n + block - 1) / block;
   trace_rays_fp64<<<static_cast<unsigned>(grid), block, 0, stream>>>(
       P, n, cells, ray_ids, dirs, out, level_steps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_states_fp64(const TraceParams& P, int64_t n, const int32_t* cells,
+                                    const uint32_t* ray_ids, uint64_t seed,
+                                    ermc_ray_state_t* out, int32_t* err, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  init_states_fp64<<<static_cast<unsigned>((n + 63) / 64), 64, 0, stream>>>(P, n, cells, ray_ids,
+                                                                            seed, out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_march_states_fp64(const TraceParams& P, int64_t n,
+                                     const ermc_ray_state_t* in, RayRecord* out,
+                                     int64_t* level_steps, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  march_states_fp64<<<static_cast<unsigned>((n + 63) / 64), 64, 0, stream>>>(P, n, in, out,
+                                                                             level_steps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_direction(int64_t n, const double* rt, const double* rp, double* out,
+                                    cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  sample_direction_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, rt, rp,
+                                                                                      out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_absorptivity(int64_t n, const double* k, const double* ds, double* out,
+                                cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  absorptivity_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(n, k, ds, out);
   return cudaGetLastError();
 }
 

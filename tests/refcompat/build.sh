@@ -13,7 +13,7 @@ OUT=$ROOT/tests/_refcompat
 mkdir -p "$OUT"
 [ -d "$REF/tests" ] || { echo "no reference tree at $REF"; exit 0; }
 g++ -std=c++20 -O1 -I"$HERE" -I"$ROOT/include" -c "$REF/tests/doctest_main.cpp" -o "$OUT/doctest_main.o"
-for T in ${TESTS:-test_solver test_spectral test_geometry test_io}; do
+for T in ${TESTS:-test_solver test_spectral test_geometry test_io test_sampling test_tracer}; do
   g++ -std=c++20 -O1 -I"$HERE" -I"$ROOT/include" -c "$REF/tests/$T.cpp" -o "$OUT/$T.o"
   g++ -o "$OUT/$T" "$OUT/$T.o" "$OUT/doctest_main.o" -L"$ROOT/paper_1810_00188_b200" -lermc_b200 \
       -Wl,-rpath,'$ORIGIN/../../paper_1810_00188_b200'

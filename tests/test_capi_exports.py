@@ -51,7 +51,10 @@ def test_struct_layouts_match_header(tmp_path):
                                               "sorting", "precision", "device"]),
               "ermc_solution_t": (capi.Solution, ["q_r", "total_steps", "wall_time"]),
               "ermc_ray_result_t": (capi.RayResult, ["q_contribution", "dir", "steps",
-                                                     "next_draw"])}
+                                                     "next_draw"]),
+              "ermc_ray_state_t": (capi.RayState, ["pos", "cell", "transmissivity", "band",
+                                                   "prefactor", "reflections", "seed",
+                                                   "cell_id", "ray_id", "next_draw"])}
     src = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(){"]
     for t, (_, fs) in fields.items():
         src.append(f'printf("{t} %zu\\n", sizeof({t}));')

@@ -1,6 +1,6 @@
 """The reference's own unit tests, unmodified, against the drop-in API.
 
-tests/refcompat/build.sh compiles proj/tests/test_{spectral,geometry,io,solver}.cpp
+tests/refcompat/build.sh compiles proj/tests/test_{spectral,geometry,io,solver,sampling,tracer}.cpp
 from the reference tree (read in place, never copied) with a doctest-compatible
 harness (tests/refcompat/doctest.h) and ermc/*.hpp shims that resolve to
 include/ermc_b200.hpp, and links them to libermc_b200.so. The binaries are
@@ -43,4 +43,20 @@ def test_reference_solver_unit_tests_pass_on_the_gpu(tmp_path, monkeypatch):
     # running on the B200 through ermc::solve.
     monkeypatch.chdir(tmp_path)
     out = _run("test_solver", timeout=1200)
+    assert "0 failed" in out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["test_sampling", "test_tracer"])
+def test_reference_per_ray_unit_tests_pass_on_the_gpu(name, tmp_path, monkeypatch):
+    # proj/tests/test_sampling.cpp and test_tracer.cpp: the keyed stream
+    # (purity, moments, chi-square), direction inversion and isotropy, CDF
+    # inversion and band frequencies, init_ray (unit R_I in the hottest cell,
+    # draw order, volume sampling), march (isothermal zero, the two-cell
+    # hand-computed exchange, black / mirror / grey walls, weight accounting,
+    # step cap, uncapped multilevel = single level bitwise, demotion) — every
+    # init_ray, march, sample_direction and absorptivity on the B200
+    # (ermc_b200_init_rays / _march_rays / _sample_direction / _absorptivity).
+    monkeypatch.chdir(tmp_path)
+    out = _run(name, timeout=1800)
     assert "0 failed" in out
