@@ -287,6 +287,27 @@ template <class T>
 struct wide_level_steps<T, std::void_t<decltype(T::kWideLevelSteps)>>
     : std::integral_constant<bool, T::kWideLevelSteps> {};
 
+// Per-level values a multigrid step reads (the level's cell words or
+// temperatures, and its eps), one 16-byte entry per level in shared memory:
+// lanes on different levels read distinct banks, and the step needs no
+// kernel-parameter load indexed by a per-lane level (those serialise in the
+// constant cache and cost a dependent load per step). Staged by the
+// multigrid kernels before pool_kernel_body's barrier.
+__shared__ ulonglong2 s_lv_hot[kMaxLevels];
+
+enum LevelData { kLvCellWords, kLvField, kLvField32 };
+__device__ __forceinline__ void stage_level_hot(const TraceParams& P, LevelData what) {
+  if (threadIdx.x < static_cast<unsigned>(P.n_levels)) {
+    const LevelDesc& L = P.lv[threadIdx.x];
+    const void* base = what == kLvCellWords ? static_cast<const void*>(L.cellw)
+                       : what == kLvField   ? static_cast<const void*>(L.field)
+                                            : static_cast<const void*>(L.field32);
+    s_lv_hot[threadIdx.x] = make_ulonglong2(reinterpret_cast<unsigned long long>(base),
+                                            static_cast<unsigned long long>(
+                                                __double_as_longlong(L.eps)));
+  }
+}
+
 // Persistent ray pool. Every lane owns one ray; when at least
 // refill_threshold lanes of a warp are idle they take the next work items
 // (positions in the dispatch order: P.perm, or cell-major (cell, ray) ids)
@@ -299,7 +320,7 @@ struct wide_level_steps<T, std::void_t<decltype(T::kWideLevelSteps)>>
 //   int init(const TraceParams&, int64_t cell, uint32_t ray)  -> DevError
 //   int step(const TraceParams&, int max_steps)               -> StepStatus
 //   double finish(const TraceParams&)       residual dump, final q
-//   int err;  int level();  int sal();  int steps();
+//   int err;  int level();  int sal(const TraceParams&);  int steps();
 template <class Tracer, bool kMulti>
 __device__ __forceinline__ void run_pool(const TraceParams& P,
                                          unsigned long long* s_steps) {
@@ -398,7 +419,7 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
             __stcs(P.q_ray + static_cast<uint64_t>(ray) * P.n_cells + cell, q);
             if (kMulti) {
               done_lvl = tr.level();
-              done_sal = static_cast<uint32_t>(tr.sal());
+              done_sal = static_cast<uint32_t>(tr.sal(P));
             } else {
               my_steps += static_cast<unsigned long long>(tr.steps());
             }

@@ -323,7 +323,7 @@ struct Fp32Tracer {
     return isfinite(tau) && isfinite(acc);
   }
   __device__ __forceinline__ int level() const { return lvl; }
-  __device__ __forceinline__ int sal() const { return sal_; }
+  __device__ __forceinline__ int sal(const TraceParams&) const { return sal_; }
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
@@ -347,7 +347,8 @@ struct Fp32Lean {
   const float4* row;
   int4* ax;  // &s_ax[0][threadIdx.x]; axis a at ax[a * kBlock32]
   int lin, band, steps_;
-  int lvl, sal_;  // kMulti: current level, steps on it
+  // kMulti: current level, and min(demotion step, max_steps) (Fp64Lean)
+  int lvl, limit_;
   uint32_t next_draw, ray_id;
   uint64_t h_cell;
   int err;
@@ -412,7 +413,7 @@ struct Fp32Lean {
     band = base.band;
     steps_ = 0;
     lvl = 0;
-    sal_ = 0;
+    if (kMulti) limit_ = level_limit(P, 0);
     next_draw = base.next_draw;
     ray_id = ray;
     h_cell = base.h_cell;
@@ -429,19 +430,33 @@ struct Fp32Lean {
     int idx[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) idx[a] = locate32(C, a, p0[a], dir[a]);
-    sal_ = 0;
+    limit_ = level_limit(P, lvl);
     setup(C, idx);
     t_cur = __ldg(C.field32 + lin);
   }
 
+  __device__ __forceinline__ int level_limit(const TraceParams& P, int l) const {
+    const int ms = static_cast<int>(P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL);
+    const int cap = P.lv[l].cap;
+    if (cap < 0 || l + 1 >= P.n_levels) return ms;
+    const long long d = static_cast<long long>(steps_) + cap;
+    return d < ms ? static_cast<int>(d) : ms;
+  }
+
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
     if (tau <= P.tol32) return kDone;
-    if (steps_ >= max_steps) return kDone;
     if (kMulti) {
-      const int cap = P.lv[lvl].cap;
-      if (cap >= 0 && sal_ >= cap && lvl + 1 < P.n_levels) demote(P);
+      if (steps_ >= limit_) {
+        if (steps_ >= max_steps) return kDone;
+        demote(P);
+      }
+    } else if (steps_ >= max_steps) {
+      return kDone;
     }
     const LevelDesc& L = P.lv[kMulti ? lvl : 0];
+    // kMulti: the level's fp32 field from the block's level table (s_lv_hot)
+    const float* field32 =
+        kMulti ? reinterpret_cast<const float*>(s_lv_hot[lvl].x) : P.lv[0].field32;
     // table record of the current cell (its T arrived during the last step)
     const float u = fmaf(t_cur, P.inv_dt32, P.u0_32);
     const int lo = min(static_cast<int>(u), P.n_temps - 2);
@@ -471,7 +486,7 @@ struct Fp32Lean {
     const bool inside = left >= 0;
     const int nlin = lin + r.y + (inside ? 0 : r.w);  // periodic image if outside
     float t_next = t_cur;
-    if (inside || P.periodic[axis]) t_next = ld_t32<kHint>(L.field32 + nlin);
+    if (inside || P.periodic[axis]) t_next = ld_t32<kHint>(field32 + nlin);
 
     const float kappa = fmaf(f, v.y, v.x);
     const float ib2n = fmaf(f, v.w, v.z);
@@ -481,7 +496,6 @@ struct Fp32Lean {
     acc = fmaf(ta, ib2n - ib1n, acc);
     tau -= ta;
     ++steps_;
-    if (kMulti) ++sal_;
 
     if (inside) {
       rp->z = left;
@@ -558,7 +572,13 @@ struct Fp32Lean {
     return isfinite(tau) && isfinite(acc);
   }
   __device__ __forceinline__ int level() const { return kMulti ? lvl : 0; }
-  __device__ __forceinline__ int sal() const { return kMulti ? sal_ : steps_; }
+  // Steps on the final level: every level below took exactly its cap.
+  __device__ __forceinline__ int sal(const TraceParams& P) const {
+    int s = steps_;
+    if (kMulti)
+      for (int l = 0; l < lvl; ++l) s -= P.lv[l].cap;
+    return s;
+  }
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
@@ -796,7 +816,7 @@ struct Fp32Brick {
     return isfinite(tau) && isfinite(acc);
   }
   __device__ __forceinline__ int level() const { return 0; }
-  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int sal(const TraceParams&) const { return steps_; }
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
@@ -835,6 +855,7 @@ template <int kMinBlocks, bool kReflect = true>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_lean_mg(const __grid_constant__ TraceParams P) {
   stage_cdfs32(P);
+  stage_level_hot(P, kLvField32);
   pool_kernel_body<Fp32Lean<0, true, kReflect>, true>(P);
 }
 

@@ -731,7 +731,7 @@ struct Fp64Fast {
   }
   __device__ __forceinline__ bool finite_state() const { return isfinite(tau); }
   __device__ __forceinline__ int level() const { return 0; }
-  __device__ __forceinline__ int sal() const { return steps_; }
+  __device__ __forceinline__ int sal(const TraceParams&) const { return steps_; }
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
@@ -811,8 +811,36 @@ struct Fp64Lean {
   int4* ax;
   int row;  // first interval record of (band, g) in iv64
   int lin, steps_;
-  int lvl, sal_;  // kMulti: current level, steps on it
+  // kMulti: current level, and the step count at which the ray next leaves
+  // the step loop's fast path: min(demotion step, max_steps) — one compare
+  // per step instead of the level's cap read through a per-lane level index.
+  int lvl, limit_;
   int err;
+
+  // kMulti: min(steps_ + cap of level l, max_steps); max_steps on the last
+  // level or one without a cap.
+  __device__ __forceinline__ int level_limit(const TraceParams& P, int l) const {
+    const int ms = static_cast<int>(P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL);
+    const int cap = P.lv[l].cap;
+    if (cap < 0 || l + 1 >= P.n_levels) return ms;
+    const long long d = static_cast<long long>(steps_) + cap;
+    return d < ms ? static_cast<int>(d) : ms;
+  }
+  // kMulti: the level's cell words (or temperatures) and eps, from the
+  // block's shared copy of the level table (lv_hot; conflict-free: one
+  // 16-byte entry per level) instead of the kernel parameters indexed by a
+  // per-lane level.
+  __device__ __forceinline__ void level_hot(const TraceParams& P, const void*& base,
+                                            double& eps) const {
+    if (kMulti) {
+      const ulonglong2 h = s_lv_hot[lvl];
+      base = reinterpret_cast<const void*>(h.x);
+      eps = __longlong_as_double(static_cast<long long>(h.y));
+    } else {
+      base = kCW ? static_cast<const void*>(P.lv[0].cellw) : static_cast<const void*>(P.lv[0].field);
+      eps = P.lv[0].eps;
+    }
+  }
 
   __device__ __forceinline__ int idx_of(const LevelDesc& L, int a) const {
     const int left = ax[a * kBlock].w;
@@ -874,7 +902,7 @@ struct Fp64Lean {
     row = (r.band * P.n_quad + r.quad) * (P.n_temps - 1);
     steps_ = 0;
     lvl = 0;
-    sal_ = 0;
+    if (kMulti) limit_ = level_limit(P, 0);
     if (!kDiet)
       ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
                                  static_cast<int>(cell), static_cast<int>(ray));
@@ -908,7 +936,7 @@ struct Fp64Lean {
       }
       idx[a] = i;
     }
-    sal_ = 0;
+    limit_ = level_limit(P, lvl);
     setup(C, idx);
     if (kCW)
       w_cur = __ldg(C.cellw + lin);
@@ -919,18 +947,22 @@ struct Fp64Lean {
 
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
     if (tau <= P.tol) return kDone;
-    if (steps_ >= max_steps) return kDone;
     if (kMulti) {
-      const int cap = P.lv[lvl].cap;
-      if (cap >= 0 && sal_ >= cap && lvl + 1 < P.n_levels) {
-        const int e = demote(P);
+      if (steps_ >= limit_) {
+        if (steps_ >= max_steps) return kDone;
+        const int e = demote(P);  // limit_ < max_steps: the level's cap is reached
         if (e != kErrNone) {
           err = e;
           return kFail;
         }
       }
+    } else if (steps_ >= max_steps) {
+      return kDone;
     }
     const LevelDesc& L = P.lv[kMulti ? lvl : 0];
+    const void* lbase;
+    double leps;
+    level_hot(P, lbase, leps);
     int lo;
     double frac;
     double4 v;  // {k_lo, k_hi, ib_lo, ib_hi}
@@ -972,15 +1004,15 @@ struct Fp64Lean {
       }
     } else {
       nlin = lin + rec.z;
-      if (!inside) nlin -= rec.z * L.n[axis];  // periodic image
+      if (kMulti ? !inside && periodic : !inside) nlin -= rec.z * L.n[axis];  // periodic image
     }
     double t_next = t_cur;
     uint64_t w_next = w_cur;
     if (inside || periodic) {
       if (kCW)
-        w_next = __ldg(L.cellw + nlin);
+        w_next = __ldg(static_cast<const uint64_t*>(lbase) + nlin);
       else
-        t_next = ld_t64<kHint>((kBrick ? L.field64b : L.field) + nlin);
+        t_next = ld_t64<kHint>((kBrick ? L.field64b : static_cast<const double*>(lbase)) + nlin);
     }
 
     // interp's frac == 0 shortcut (spectral.cpp:179-205) needs no select here:
@@ -994,7 +1026,7 @@ struct Fp64Lean {
     q += P.qe * tau * alpha * div_rcp(ib2 - ib1, ib1, rib1) * pref;
     tau *= 1.0 - alpha;
 
-    const double advance = ds + L.eps;
+    const double advance = ds + leps;
     if (kPos) {
       pos[0] += advance * dir[0];
       pos[1] += advance * dir[1];
@@ -1007,7 +1039,6 @@ struct Fp64Lean {
     for (int a = 0; a < 3; ++a)
       if (a == axis) tn[a] += td;
     ++steps_;
-    if (kMulti) ++sal_;
 
     if (inside) {
       rp->w = left;
@@ -1094,7 +1125,13 @@ struct Fp64Lean {
   }
   __device__ __forceinline__ bool finite_state() const { return isfinite(tau); }
   __device__ __forceinline__ int level() const { return kMulti ? lvl : 0; }
-  __device__ __forceinline__ int sal() const { return kMulti ? sal_ : steps_; }
+  // Steps on the final level: every level below took exactly its cap.
+  __device__ __forceinline__ int sal(const TraceParams& P) const {
+    int s = steps_;
+    if (kMulti)
+      for (int l = 0; l < lvl; ++l) s -= P.lv[l].cap;
+    return s;
+  }
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
@@ -1116,7 +1153,7 @@ struct Fp64Tracer {
     return isfinite(r.tau);
   }
   __device__ __forceinline__ int level() const { return r.level; }
-  __device__ __forceinline__ int sal() const { return r.sal; }
+  __device__ __forceinline__ int sal(const TraceParams&) const { return r.sal; }
   __device__ __forceinline__ int steps() const { return r.steps; }
 };
 struct Fp64Multi : Fp64Tracer {
@@ -1158,6 +1195,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
   stage_sampling(P, s_dyn + kLeanRecs64 * kBlock);
+  stage_level_hot(P, kCW ? kLvCellWords : kLvField);
   pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
 }
 
