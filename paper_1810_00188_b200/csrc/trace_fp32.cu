@@ -485,8 +485,8 @@ struct Fp32Lean {
     const int left = r.z - 1;
     const bool inside = left >= 0;
     const int nlin = lin + r.y + (inside ? 0 : r.w);  // periodic image if outside
-    float t_next = t_cur;
-    if (inside || P.periodic[axis]) t_next = ld_t32<kHint>(field32 + nlin);
+    // next cell's temperature straight into t_cur (see Fp64Lean::step)
+    t_cur = ld_t32<kHint>(field32 + ((inside || P.periodic[axis]) ? nlin : lin));
 
     const float kappa = fmaf(f, v.y, v.x);
     const float ib2n = fmaf(f, v.w, v.z);
@@ -500,7 +500,6 @@ struct Fp32Lean {
     if (inside) {
       rp->z = left;
       lin = nlin;
-      t_cur = t_next;
       return kContinue;
     }
     if (P.periodic[axis]) {
@@ -511,7 +510,6 @@ struct Fp32Lean {
       for (int a = 0; a < 3; ++a)
         if (a == axis) p0[a] += r.y > 0 ? -ext : ext;
       lin = nlin;
-      t_cur = t_next;
       return kContinue;
     }
     // wall exchange (tracer.cpp:155-165); the ray stays in its cell
@@ -720,17 +718,15 @@ struct Fp32Brick {
     // the step leaves its brick when the cells-left counter is a multiple of kB
     const int near = kB == 2 ? (4 >> axis) : (16 >> (2 * axis));
     int nlin = lin + ((left0 & (kB - 1)) ? (far > 0 ? near : -near) : far);
-    float t_next = t_cur;
-    if (inside) {
-      t_next = ld_t32<kHint>(L.field32b + nlin);
-    } else if (periodic) {
+    if (!inside && periodic) {
       int idx[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
         idx[a] = a == axis ? (far > 0 ? 0 : L.n[a] - 1) : idx_of(L, a);
       nlin = brick_index_b<kB>(L, idx[0], idx[1], idx[2]);
-      t_next = ld_t32<kHint>(L.field32b + nlin);
     }
+    // next cell's temperature straight into t_cur (see Fp64Lean::step)
+    t_cur = ld_t32<kHint>(L.field32b + ((inside || periodic) ? nlin : lin));
 
     const float kappa = fmaf(f, v.y, v.x);
     const float ib2n = fmaf(f, v.w, v.z);
@@ -744,7 +740,6 @@ struct Fp32Brick {
     if (inside) {
       *lp = left;
       lin = nlin;
-      t_cur = t_next;
       return kContinue;
     }
     if (periodic) {
@@ -755,7 +750,6 @@ struct Fp32Brick {
       for (int a = 0; a < 3; ++a)
         if (kPos && a == axis) p0[a] += far > 0 ? -ext : ext;
       lin = nlin;
-      t_cur = t_next;
       return kContinue;
     }
     // wall exchange (tracer.cpp:155-165); the ray stays in its cell

@@ -1006,14 +1006,17 @@ struct Fp64Lean {
       nlin = lin + rec.z;
       if (kMulti ? !inside && periodic : !inside) nlin -= rec.z * L.n[axis];  // periodic image
     }
-    double t_next = t_cur;
-    uint64_t w_next = w_cur;
-    if (inside || periodic) {
-      if (kCW)
-        w_next = __ldg(static_cast<const uint64_t*>(lbase) + nlin);
-      else
-        t_next = ld_t64<kHint>((kBrick ? L.field64b : static_cast<const double*>(lbase)) + nlin);
-    }
+    // The next cell's word (temperature) is loaded straight into w_cur
+    // (t_cur): this step's decode has consumed it, so the gather stays in
+    // flight until the next step's decode. Loaded into a second register and
+    // moved at the end of the step, every step waited for its own gather at
+    // the move (ncu r2aj: 14 % of the stall samples). A wall step reloads
+    // its own cell.
+    const int ld_lin = (inside || periodic) ? nlin : lin;
+    if (kCW)
+      w_cur = __ldg(static_cast<const uint64_t*>(lbase) + ld_lin);
+    else
+      t_cur = ld_t64<kHint>((kBrick ? L.field64b : static_cast<const double*>(lbase)) + ld_lin);
 
     // interp's frac == 0 shortcut (spectral.cpp:179-205) needs no select here:
     // a + 0 * (b - a) == a for finite table values (k is validated finite; a
@@ -1043,8 +1046,6 @@ struct Fp64Lean {
     if (inside) {
       rp->w = left;
       lin = nlin;
-      t_cur = t_next;
-      w_cur = w_next;
       return kContinue;
     }
     if (periodic) {
@@ -1054,8 +1055,6 @@ struct Fp64Lean {
       for (int a = 0; a < 3; ++a)
         if (kPos && a == axis) pos[a] += rec.z > 0 ? -ext : ext;
       lin = nlin;
-      t_cur = t_next;
-      w_cur = w_next;
       return kContinue;
     }
     // Wall exchange, absorption or reflection (tracer.cpp:155-184); the ray
