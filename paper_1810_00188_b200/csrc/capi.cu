@@ -808,6 +808,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
   P.qe = qe;
   P.tol = c.tolerance;
   P.max_steps = c.max_steps;
+  ermc_dev::set_level_budgets(P);
   P.specular = c.specular_walls;
   P.volume_sampling = c.volume_sampling;
   P.h_seed = mix64_host(c.seed + 0x9e3779b97f4a7c15ULL);
@@ -1790,6 +1791,7 @@ int ermc_b200_march_rays(int32_t n_levels, const ermc_grid_t* grids,
     P.qe = q_emission;
     P.tol = tolerance;
     P.max_steps = max_steps;
+    ermc_dev::set_level_budgets(P);
     P.specular = specular;
     DevBuf<ermc_ray_state_t> din;
     DevBuf<ermc_dev::RayRecord> drec;

@@ -48,6 +48,11 @@ struct LevelDesc {
   // (lo << cw_shift) | m, where lo is the reference lookup's interval and
   // m * 2^-cw_scale_exp == T - t[lo] exactly.
   const uint64_t* cellw;
+  // Step budget of a ray on this level (set_level_budgets): the steps it can
+  // take here before it demotes or reaches max_steps, counted from its first
+  // step on the level; budget_demotes = 1 when the budget ends in a demotion.
+  int32_t budget;
+  int32_t budget_demotes;
 };
 
 // Error codes raised on the device; the host re-traces the failing ray
@@ -141,6 +146,31 @@ struct TraceParams {
   unsigned long long* err_key;          // ~(min failing work item) (0 = none)
   int32_t* err_code;
 };
+
+// Per-level step budgets (LevelDesc::budget) from the caps and max_steps, in
+// the order of the reference's checks (tracer.cpp:88-101): a ray stops at
+// max_steps before it demotes. Host side, after the levels and max_steps are
+// set.
+inline void set_level_budgets(TraceParams& P) {
+  const long long ms = P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL;
+  long long start = 0;  // steps taken on the finer levels when a ray arrives
+  for (int l = 0; l < P.n_levels; ++l) {
+    LevelDesc& L = P.lv[l];
+    const bool capped = L.cap >= 0 && l + 1 < P.n_levels;
+    const long long left = ms > start ? ms - start : 0;
+    const bool demotes = capped && start + L.cap < ms;
+    L.budget = static_cast<int32_t>(demotes ? L.cap : left);
+    L.budget_demotes = demotes ? 1 : 0;
+    if (!demotes) {  // no ray gets past this level
+      for (int k = l + 1; k < P.n_levels; ++k) {
+        P.lv[k].budget = 0;
+        P.lv[k].budget_demotes = 0;
+      }
+      break;
+    }
+    start += L.cap;
+  }
+}
 
 // Full-field output buffers of the fused reduce + all-gather (K2 scatter).
 constexpr int kMaxScatter = 8;

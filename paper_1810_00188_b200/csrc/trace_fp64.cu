@@ -810,22 +810,14 @@ struct Fp64Lean {
   uint64_t w_cur;  // kCW: the current cell's word
   int4* ax;
   int row;  // first interval record of (band, g) in iv64
-  int lin, steps_;
-  // kMulti: current level, and the step count at which the ray next leaves
-  // the step loop's fast path: min(demotion step, max_steps) — one compare
-  // per step instead of the level's cap read through a per-lane level index.
-  int lvl, limit_;
+  int lin;
+  // Single level: steps taken. kMulti: steps left of the current level's
+  // budget (LevelDesc::budget: until the demotion or max_steps) — one
+  // register and one compare per step instead of a step count, a limit and
+  // the level's cap read through a per-lane level index.
+  int steps_;
+  int lvl;  // kMulti: current level
   int err;
-
-  // kMulti: min(steps_ + cap of level l, max_steps); max_steps on the last
-  // level or one without a cap.
-  __device__ __forceinline__ int level_limit(const TraceParams& P, int l) const {
-    const int ms = static_cast<int>(P.max_steps < 0x7fffffffLL ? P.max_steps : 0x7fffffffLL);
-    const int cap = P.lv[l].cap;
-    if (cap < 0 || l + 1 >= P.n_levels) return ms;
-    const long long d = static_cast<long long>(steps_) + cap;
-    return d < ms ? static_cast<int>(d) : ms;
-  }
   // kMulti: the level's cell words (or temperatures) and eps, from the
   // block's shared copy of the level table (lv_hot; conflict-free: one
   // 16-byte entry per level) instead of the kernel parameters indexed by a
@@ -900,9 +892,8 @@ struct Fp64Lean {
     rib1 = 1.0 / r.ib1;
     pref = r.pref;
     row = (r.band * P.n_quad + r.quad) * (P.n_temps - 1);
-    steps_ = 0;
     lvl = 0;
-    if (kMulti) limit_ = level_limit(P, 0);
+    steps_ = kMulti ? P.lv[0].budget : 0;
     if (!kDiet)
       ax[3 * kBlock] = make_int4(r.band, static_cast<int>(r.next_draw),
                                  static_cast<int>(cell), static_cast<int>(ray));
@@ -936,7 +927,7 @@ struct Fp64Lean {
       }
       idx[a] = i;
     }
-    limit_ = level_limit(P, lvl);
+    steps_ = C.budget;
     setup(C, idx);
     if (kCW)
       w_cur = __ldg(C.cellw + lin);
@@ -948,9 +939,9 @@ struct Fp64Lean {
   __device__ __forceinline__ int step(const TraceParams& P, int max_steps) {
     if (tau <= P.tol) return kDone;
     if (kMulti) {
-      if (steps_ >= limit_) {
-        if (steps_ >= max_steps) return kDone;
-        const int e = demote(P);  // limit_ < max_steps: the level's cap is reached
+      if (steps_ <= 0) {  // the level's budget is spent: demote or stop
+        if (!P.lv[lvl].budget_demotes) return kDone;
+        const int e = demote(P);
         if (e != kErrNone) {
           err = e;
           return kFail;
@@ -1041,7 +1032,7 @@ struct Fp64Lean {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
       if (a == axis) tn[a] += td;
-    ++steps_;
+    steps_ += kMulti ? -1 : 1;
 
     if (inside) {
       rp->w = left;
@@ -1126,12 +1117,9 @@ struct Fp64Lean {
   __device__ __forceinline__ int level() const { return kMulti ? lvl : 0; }
   // Steps on the final level: every level below took exactly its cap.
   __device__ __forceinline__ int sal(const TraceParams& P) const {
-    int s = steps_;
-    if (kMulti)
-      for (int l = 0; l < lvl; ++l) s -= P.lv[l].cap;
-    return s;
+    return kMulti ? P.lv[lvl].budget - steps_ : steps_;
   }
-  __device__ __forceinline__ int steps() const { return steps_; }
+  __device__ __forceinline__ int steps() const { return steps_; }  // single level
 };
 
 struct Fp64Tracer {
