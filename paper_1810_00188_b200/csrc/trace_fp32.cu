@@ -30,15 +30,14 @@ namespace {
 constexpr int kBlock32 = 128;
 
 // 1 - exp(-x) for x >= 0: Taylor near 0 (no cancellation), ex2 otherwise.
+// Both forms evaluated and selected: lanes of a warp straddle 0.125.
 __device__ __forceinline__ float absorb32(float x) {
-  if (x < 0.125f) {
-    float p = fmaf(x, -1.0f / 120.0f, 1.0f / 24.0f);
-    p = fmaf(x, -p, 1.0f / 6.0f);
-    p = fmaf(x, -p, 0.5f);
-    p = fmaf(x, -p, 1.0f);
-    return x * p;
-  }
-  return 1.0f - __expf(-x);
+  const float big = 1.0f - __expf(-x);
+  float p = fmaf(x, -1.0f / 120.0f, 1.0f / 24.0f);
+  p = fmaf(x, -p, 1.0f / 6.0f);
+  p = fmaf(x, -p, 0.5f);
+  p = fmaf(x, -p, 1.0f);
+  return x < 0.125f ? x * p : big;
 }
 
 // locate (geometry.cpp:112-138) of a demoted ray on level C, axis a. The
