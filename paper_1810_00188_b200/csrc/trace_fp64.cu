@@ -748,6 +748,11 @@ __constant__ double kEm1Coef[12] = {
     1.0 / 40320, 1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800,
     1.0 / 479001600, 1.0 / 6227020800.0};
 
+// kJ0Path: a separate branch for j = 0 (|x| < ln2 / 2, most steps and
+// warp-uniform in practice) that skips the reduction — r = x exactly there
+// (fma(0, c, x)), so the bits are the same. Single-level tracers only:
+// +0.4 % there, −5.7 % in the larger multigrid kernel (r2ax).
+template <bool kJ0Path = false>
 __device__ __forceinline__ double expm1_lean(double x) {
   if (!(x >= -40.0 && x <= 0.5)) {
     if (x < -40.0) return -1.0;  // |expm1(x) + 1| < 2^-57
@@ -755,6 +760,13 @@ __device__ __forceinline__ double expm1_lean(double x) {
   }
   const double magic = 6755399441055744.0;  // 1.5 * 2^52
   const double t = fma(x, 1.4426950408889634074, magic);
+  const int ji = __double2loint(t);
+  if (kJ0Path && ji == 0) {
+    double p = kEm1Coef[11];
+#pragma unroll
+    for (int i = 10; i >= 0; --i) p = fma(p, x, kEm1Coef[i]);
+    return fma(x * x, p, x);
+  }
   const double j = t - magic;
   double r = fma(j, -6.93147180369123816490e-01, x);
   r = fma(j, -1.90821492927058770002e-10, r);
@@ -762,8 +774,7 @@ __device__ __forceinline__ double expm1_lean(double x) {
 #pragma unroll
   for (int i = 10; i >= 0; --i) p = fma(p, r, kEm1Coef[i]);
   const double e = fma(r * r, p, r);
-  const int ji = __double2loint(t);
-  if (ji == 0) return e;
+  if (!kJ0Path && ji == 0) return e;
   const double sc = __hiloint2double((ji + 1023) << 20, 0);
   return fma(sc, e, sc - 1.0);
 }
@@ -1015,7 +1026,7 @@ struct Fp64Lean {
     // are re-traced by the reference-order debug tracer for the error).
     const double kappa = v.x + frac * (v.y - v.x);
     const double ib2 = v.z + frac * (v.w - v.z);
-    const double alpha = -expm1_lean(-kappa * ds);
+    const double alpha = -expm1_lean<!kMulti>(-kappa * ds);
     last_ib2 = ib2;
     q += P.qe * tau * alpha * div_rcp(ib2 - ib1, ib1, rib1) * pref;
     tau *= 1.0 - alpha;
