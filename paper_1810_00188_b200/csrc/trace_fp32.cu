@@ -813,11 +813,11 @@ struct Fp32Brick {
   __device__ __forceinline__ int steps() const { return steps_; }
 };
 
-template <int kMinBlocks, int kHint, bool kPos = true, int kB = 2>
+template <int kMinBlocks, int kHint, bool kPos = true, int kB = 2, int kInner = 0>
 __global__ void __launch_bounds__(kBlock32, kMinBlocks)
     trace_pool_fp32_brick(const __grid_constant__ TraceParams P) {
   stage_cdfs32(P);
-  pool_kernel_body<Fp32Brick<kHint, kPos, kB>, false>(P);
+  pool_kernel_body<Fp32Brick<kHint, kPos, kB>, false, kInner>(P);
 }
 
 // Converts the fp64 k-fastest field to the fp32 micro-brick layout (edge b).
@@ -914,8 +914,11 @@ TraceFn32 fp32_kernel(const TraceParams& P, int min_blocks) {
   }
   if (fp32_lean(P) && P.brick) {
     if (!P.track_pos && P.brick == 4) return trace_pool_fp32_brick<8, 0, false, 4>;
-    if (!P.track_pos)
+    if (!P.track_pos) {
+      if (eight && P.inner_steps == 48)  // the default window compiled in
+        return trace_pool_fp32_brick<8, 0, false, 2, 48>;
       return eight ? trace_pool_fp32_brick<8, 0, false> : trace_pool_fp32_brick<6, 0, false>;
+    }
     return eight ? trace_pool_fp32_brick<8, 0> : trace_pool_fp32_brick<6, 0>;
   }
   if (fp32_lean(P)) return eight ? trace_pool_fp32_lean<8, 0> : trace_pool_fp32_lean<6, 0>;

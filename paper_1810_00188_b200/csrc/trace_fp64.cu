@@ -1174,7 +1174,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     pool_kernel_body<Fp64Fast, false>(P);
 }
 
-template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = false>
+template <int kMinBlocks, int kHint, bool kBrick, bool kPos = true, bool kCW = false,
+          int kInner = 0>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
@@ -1184,7 +1185,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
     else
       stage_sampling(P, s_dyn + kLeanRecs64 * kBlock);
   }
-  pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false>(P);
+  pool_kernel_body<Fp64Lean<kHint, kBrick, kPos, false, kPos, kCW>, false, kInner>(P);
 }
 
 // Multigrid variant of the lean tracer (n_levels > 1).
@@ -1627,10 +1628,14 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
       return min_blocks >= 7 ? trace_pool_fp64_lean_mg<7, true, true>
                              : trace_pool_fp64_lean_mg<6, true, true>;
     }
-    if (!P.track_pos)
+    if (!P.track_pos) {
+      // the bench kernel with its default window compiled in (kInner = 32)
+      if (min_blocks == 7 && P.inner_steps == 32)
+        return trace_pool_fp64_lean<7, 0, false, false, true, 32>;
       return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, false, true>
              : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, false, true>
                                : trace_pool_fp64_lean<6, 0, false, false, true>;
+    }
     return min_blocks == 8   ? trace_pool_fp64_lean<8, 0, false, true, true>
            : min_blocks == 7 ? trace_pool_fp64_lean<7, 0, false, true, true>
                              : trace_pool_fp64_lean<6, 0, false, true, true>;
