@@ -402,9 +402,10 @@ __device__ __forceinline__ void run_pool(const TraceParams& P,
       // whose ray ends early idles for < inner_steps iterations.
       int st = kContinue;
       if constexpr (kMulti) {
+        const int inner = kInner > 0 ? kInner : P.inner_steps;
         // not unrolled: the demotion makes the step body large (i-cache)
 #pragma unroll 1
-        for (int s = 0; s < P.inner_steps && st == kContinue; ++s)
+        for (int s = 0; s < inner && st == kContinue; ++s)
           st = tr.step(P, max_steps);
       } else {
         const int inner = kInner > 0 ? kInner : P.inner_steps;  // +1.5 % fp64 (r2az)

@@ -1189,13 +1189,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks)
 }
 
 // Multigrid variant of the lean tracer (n_levels > 1).
-template <int kMinBlocks, bool kReflect = true, bool kCW = false>
+template <int kMinBlocks, bool kReflect = true, bool kCW = false, int kInner = 0>
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
     trace_pool_fp64_lean_mg(const __grid_constant__ TraceParams P) {
   extern __shared__ int4 s_dyn[];
   stage_sampling(P, s_dyn + kLeanRecs64 * kBlock);
   stage_level_hot(P, kCW ? kLvCellWords : kLvField);
-  pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true>(P);
+  pool_kernel_body<Fp64Lean<0, false, true, true, kReflect, kCW>, true, kInner>(P);
 }
 
 // Cell words of one level (TraceParams::cw_*), with the reference lookup
@@ -1621,6 +1621,8 @@ TraceFn fp64_kernel_p(const TraceParams& P, int min_blocks) {
   min_blocks = min(max(min_blocks, 6), 8);
   if (P.cellw) {
     if (P.n_levels > 1) {
+      if (!P.track_pos && min_blocks == 7 && P.inner_steps == 64)  // 6+ levels' window
+        return trace_pool_fp64_lean_mg<7, false, true, 64>;
       if (!P.track_pos)
         return min_blocks >= 8   ? trace_pool_fp64_lean_mg<8, false, true>
                : min_blocks == 7 ? trace_pool_fp64_lean_mg<7, false, true>
