@@ -803,6 +803,7 @@ void prepare(ermc_session* s, Prepared& pr, double t_max, double qe,
     P.div_rays = fast_div(static_cast<uint32_t>(c.rays_per_cell));
     P.div_nyz = fast_div(nyz < (1ull << 31) ? static_cast<uint32_t>(nyz) : 1u);
     P.div_nz = fast_div(static_cast<uint32_t>(g0.nz));
+    P.div_row = fast_div(static_cast<uint32_t>(std::max(1, s->view.nq * (s->view.nt - 1))));
   }
   P.ib_max = s->d_ibmax.p;
   P.qe = qe;

@@ -127,6 +127,7 @@ struct TraceParams {
 
   // ---- per-ray setup helpers (bitwise the reference's arithmetic) ----
   FastDiv div_rays, div_nyz, div_nz;  // work id -> (cell, ray); level-0 cell decode
+  FastDiv div_row;  // interval row -> band: n_quad * (n_temps - 1)
   const double2* pref_den;   // [n_bands*n_quad] {k(n,g,T_max) Ib(n,T_max), RN(1 / that)}
 
   // ---- work decomposition ----

@@ -1063,7 +1063,7 @@ struct Fp64Lean {
     // stays in its boundary cell (its record still says 0 cells left).
     const bool at_hi = rec.z > 0;
     const int face = 2 * axis + (at_hi ? 1 : 0);
-    const int4 r3 = kDiet ? make_int4(row / (P.n_quad * (P.n_temps - 1)), 0, 0, 0)
+    const int4 r3 = kDiet ? make_int4(static_cast<int>(fdiv(static_cast<uint32_t>(row), P.div_row)), 0, 0, 0)
                           : ax[3 * kBlock];
     const double ew = P.wall_eps[face];
     const double ib_w = __ldg(P.wall_ib + face * P.n_bands + r3.x);
