@@ -985,6 +985,7 @@ struct Fp64Lean {
       ds = tn[2];
       axis = 2;
     }
+    const double t_axis = ds;  // tn[axis]
     if (ds < 0.0) ds = 0.0;
 
     int4* rp = ax + axis * kBlock;
@@ -1037,12 +1038,11 @@ struct Fp64Lean {
       pos[1] += advance * dir[1];
       pos[2] += advance * dir[2];
     }
-    tn[0] -= advance;
-    tn[1] -= advance;
-    tn[2] -= advance;
+    // tn[axis] - advance + td computed once from the selected value (same
+    // operands, same bits) instead of three speculative adds and selects
+    const double t_new = (t_axis - advance) + td;
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      if (a == axis) tn[a] += td;
+    for (int a = 0; a < 3; ++a) tn[a] = a == axis ? t_new : tn[a] - advance;
     steps_ += kMulti ? -1 : 1;
 
     if (inside) {
