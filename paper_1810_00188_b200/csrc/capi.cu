@@ -343,7 +343,8 @@ struct Tune {
   int cdf_smem = 1;    // stage the sampling CDFs in shared memory (lean kernels)
   int sort_tile_items = 1 << 16;
   // cubic sort tiles (edge in cells; 0 = linear tiles, -1 = the largest edge
-  // with edge^3 * R <= 2^16: 10 at R = 64, measured +0.75 % over linear, r2bk)
+  // with edge^3 * R <= 2^16 for single-level solves (10 at R = 64: +0.6 %
+  // over linear, r2bk/r2bl), linear for multigrid (−1.2 % there, r2bn))
   int sort_block = -1;
   int sort_dirs = 32;  // direction bins inside each spectral row (1, 8, 32: +1.9 % at 32)
   int cellw = 1;       // fp64 lean tracers read precomputed cell words (trace_fp64.cu)
@@ -1047,7 +1048,9 @@ void session_enqueue(ermc_session* s, int64_t lo, int64_t hi, double* d_q,
   const int tile_cells = std::max(
       1, std::min(tune().sort_tile_items, ermc_dev::sort_max_tile_items()) / R);
   int sort_block = tune().sort_block;
-  if (sort_block < 0) {  // auto: the largest cube of whole cells in a tile
+  if (sort_block < 0 && s->config.n_levels > 1) {
+    sort_block = 0;  // multigrid: the cubic tiles' slower sort is not repaid (r2bn)
+  } else if (sort_block < 0) {  // auto: the largest cube of whole cells in a tile
     sort_block = 1;
     while (static_cast<int64_t>(sort_block + 1) * (sort_block + 1) * (sort_block + 1) * R <=
            (int64_t(1) << 16))
