@@ -19,6 +19,8 @@ for prec in (capi.FP64, capi.FP32):
     capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec, n_devices=2))
     capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec, n_levels=4,
                                               steps_per_level=2))  # black-wall multigrid tracers
+g, t, b, m = W.channel_case(32, "nongrey16")[:4]    # 6 levels: the 64-step multigrid window
+capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=2, seed=3, n_levels=6, steps_per_level=2))
 g, t, b, m = W.channel_case(16, "nongrey119")[:4]   # guides-only CDF staging
 for prec in (capi.FP64, capi.FP32):
     capi.solve(g, t, b, m, capi.config_struct(rays_per_cell=8, seed=3, precision=prec))
