@@ -44,6 +44,6 @@ print("sanitizer cases done")
 PY
 sed -i "s#ROOT#$PWD#g" /tmp/san_case.py
 timeout 1500 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_memcheck.txt 2>&1; echo "memcheck rc=$?" >> $OUT/sanitize_memcheck.txt
-ERMC_SORT_BLOCK=8 timeout 1500 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_memcheck_blk.txt 2>&1; echo "memcheck rc=$?" >> $OUT/sanitize_memcheck_blk.txt
+ERMC_SORT_BLOCK=0 timeout 1500 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_memcheck_blk.txt 2>&1; echo "memcheck rc=$?" >> $OUT/sanitize_memcheck_blk.txt
 timeout 1500 $CS --tool racecheck --error-exitcode 9 python /tmp/san_case.py > $OUT/sanitize_racecheck.txt 2>&1; echo "racecheck rc=$?" >> $OUT/sanitize_racecheck.txt
 tail -n 3 $OUT/sanitize_memcheck.txt $OUT/sanitize_memcheck_blk.txt $OUT/sanitize_racecheck.txt
